@@ -1,0 +1,331 @@
+// K1: GPU Tiled-CSL encoder, bit-exact with tcsl::encode
+// (reference: proj/src/tcsl_format.cpp:36-124, layout proj/include/tcsl/tcsl_format.hpp:12-54).
+//
+// The reference emits each tile's nonzeros with a sequential greedy loop:
+// "pull from the bank bucket with the most entries left, smallest bank id on
+// ties, FIFO inside a bucket" (tcsl_format.cpp:81-97). That loop is a pure
+// function of the 32 bucket sizes c_b and each entry's FIFO index k inside its
+// bucket: the entry is emitted when its bucket has L = c_b - k entries left,
+// and every entry with a larger "level" L' > L (from any bucket) or the same
+// level in a smaller bank precedes it. Hence
+//     pos = F(L) + popc(Mask(L) & ((1 << b) - 1)),
+//     F(L) = sum_b' max(0, c_b' - L),  Mask(L) = {b' : c_b' >= L},
+// a closed form every thread evaluates independently.
+// Padding: +0.0 entries at the tile's first (32 - nnz % 32) % 32 zero
+// positions in row-major order, fringe included (tcsl_format.cpp:103-119).
+//
+// Two passes: encode_count_kernel -> exclusive scan (CUB) -> encode_emit_kernel.
+#include <cub/cub.cuh>
+
+#include "tcsl_internal.cuh"
+
+namespace tcslk {
+
+namespace {
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// One block per tile: number of nonzero (bit pattern & 0x7FFF != 0) elements
+// inside the matrix, rounded up to whole 32-entry groups.
+__global__ void __launch_bounds__(256) encode_count_kernel(const uint16_t* __restrict__ w, uint32_t m,
+                                                           uint32_t k, int m_tb, int k_tb, int tiles_k,
+                                                           uint32_t* __restrict__ counts) {
+  const uint32_t tile = blockIdx.x;
+  const long long r0 = static_cast<long long>(tile / tiles_k) * m_tb;
+  const int c0 = static_cast<int>(tile % tiles_k) * k_tb;
+  const int x_end = static_cast<int>(min(static_cast<long long>(m_tb), static_cast<long long>(m) - r0));
+  const int y_end = min(k_tb, static_cast<int>(k) - c0);
+  uint32_t cnt = 0;
+  if ((k & 7u) == 0) {
+    // 16-byte vector loads: rows start 16-B aligned because k % 8 == 0 and c0 % 8 == 0.
+    const int vpr = (y_end + 7) >> 3;
+    const int total = x_end * vpr;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int x = i / vpr, v = i - x * vpr;
+      const uint16_t* p = w + (r0 + x) * k + c0 + v * 8;
+      if (v * 8 + 8 <= y_end) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
+        const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cnt += ((wd[e] & 0x7FFFu) != 0) + ((wd[e] & 0x7FFF0000u) != 0);
+      } else {
+        for (int y = v * 8; y < y_end; ++y) cnt += (p[y - v * 8] & 0x7FFFu) != 0;
+      }
+    }
+  } else {
+    const int total = x_end * y_end;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int x = i / y_end, y = i - x * y_end;
+      cnt += (w[(r0 + x) * k + c0 + y] & 0x7FFFu) != 0;
+    }
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  __shared__ uint32_t part[32];
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) part[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t s = 0;
+    for (int i = 0; i < (blockDim.x >> 5); ++i) s += part[i];
+    counts[tile] = (s + 31u) & ~31u;
+  }
+}
+
+struct EmitLayout {
+  int items;     // m_tb * ceil(k_tb / 64): one (row, 64-column chunk) per warp step
+  int max_level; // m_tb * k_tb / 32: the largest possible bank count
+  bool stage;    // stage the tile's entries in smem (tile_elems <= 8192)
+  size_t cnt4, nzz, bpre, npre, zpre, cb, fl, ml, stg, bytes;
+};
+
+__host__ __device__ inline EmitLayout emit_layout(int m_tb, int k_tb) {
+  EmitLayout L{};
+  const int nch = (k_tb + 63) / 64;
+  L.items = m_tb * nch;
+  L.max_level = m_tb * k_tb / 32;
+  L.stage = m_tb * k_tb <= 8192;
+  size_t o = 0;
+  L.cnt4 = o; o += 4ull * L.items;
+  L.nzz = o;  o += 4ull * L.items;
+  L.npre = o; o += 4ull * L.items;
+  L.zpre = o; o += 4ull * L.items;
+  L.bpre = o; o += 8ull * L.items;
+  L.cb = o;   o += 4ull * 32 + 16;
+  L.fl = o;   o += 4ull * (L.max_level + 2);
+  L.ml = o;   o += 4ull * (L.max_level + 2);
+  o = (o + 15) & ~size_t(15);
+  L.stg = o;  o += L.stage ? 4ull * m_tb * k_tb : 0;
+  L.bytes = o;
+  return L;
+}
+
+struct Pair {
+  uint32_t v0, v1;  // element bits (0 when outside)
+  bool nz0, nz1;    // numerically nonzero inside the matrix
+  bool in0, in1;    // position exists inside the m_tb x k_tb tile
+};
+
+__device__ __forceinline__ Pair load_pair(const uint16_t* __restrict__ w, uint32_t k, long long r0, int c0,
+                                          int x, int y0, int x_end, int y_end, int k_tb) {
+  Pair p;
+  p.in0 = y0 < k_tb;
+  p.in1 = y0 + 1 < k_tb;
+  const bool val0 = x < x_end && y0 < y_end;
+  const bool val1 = x < x_end && y0 + 1 < y_end;
+  p.v0 = p.v1 = 0;
+  if (val0) {
+    const uint16_t* src = w + (r0 + x) * k + c0 + y0;
+    if (val1 && ((reinterpret_cast<uintptr_t>(src) & 3u) == 0)) {
+      const uint32_t both = __ldg(reinterpret_cast<const uint32_t*>(src));
+      p.v0 = both & 0xFFFFu;
+      p.v1 = both >> 16;
+    } else {
+      p.v0 = __ldg(src);
+      if (val1) p.v1 = __ldg(src + 1);
+    }
+  }
+  p.nz0 = (p.v0 & 0x7FFFu) != 0;
+  p.nz1 = (p.v1 & 0x7FFFu) != 0;
+  return p;
+}
+
+// One block (8 warps) per tile. See the file comment for the closed form.
+__global__ void __launch_bounds__(256) encode_emit_kernel(const uint16_t* __restrict__ w, uint32_t m,
+                                                          uint32_t k, int m_tb, int k_tb, int tiles_k,
+                                                          int reorder, const uint32_t* __restrict__ offsets,
+                                                          uint32_t* __restrict__ entries, int* err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const EmitLayout lay = emit_layout(m_tb, k_tb);
+  uint32_t* cnt4 = reinterpret_cast<uint32_t*>(smem + lay.cnt4);
+  uint32_t* nzz = reinterpret_cast<uint32_t*>(smem + lay.nzz);
+  uint32_t* npre = reinterpret_cast<uint32_t*>(smem + lay.npre);
+  uint32_t* zpre = reinterpret_cast<uint32_t*>(smem + lay.zpre);
+  uint16_t* bpre = reinterpret_cast<uint16_t*>(smem + lay.bpre);
+  uint32_t* cb = reinterpret_cast<uint32_t*>(smem + lay.cb);
+  uint32_t* fl = reinterpret_cast<uint32_t*>(smem + lay.fl);
+  uint32_t* ml = reinterpret_cast<uint32_t*>(smem + lay.ml);
+  uint32_t* stg = reinterpret_cast<uint32_t*>(smem + lay.stg);
+
+  const uint32_t tile = blockIdx.x;
+  const long long r0 = static_cast<long long>(tile / tiles_k) * m_tb;
+  const int c0 = static_cast<int>(tile % tiles_k) * k_tb;
+  const int x_end = static_cast<int>(min(static_cast<long long>(m_tb), static_cast<long long>(m) - r0));
+  const int y_end = min(k_tb, static_cast<int>(k) - c0);
+  const int nch = (k_tb + 63) / 64;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const uint32_t lt = lanemask_lt();
+
+  // ---- pass A: per (row, chunk) item, per-bank-column counts and nz / zero counts
+  for (int it = warp; it < lay.items; it += nwarps) {
+    const int x = it / nch, ch = it - x * nch;
+    const Pair p = load_pair(w, k, r0, c0, x, ch * 64 + 2 * lane, x_end, y_end, k_tb);
+    const uint32_t b0 = __ballot_sync(0xffffffffu, p.nz0), b1 = __ballot_sync(0xffffffffu, p.nz1);
+    const uint32_t z0 = __ballot_sync(0xffffffffu, p.in0 && !p.nz0);
+    const uint32_t z1 = __ballot_sync(0xffffffffu, p.in1 && !p.nz1);
+    if (lane == 0) {
+      uint32_t c4 = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t mj = 0x11111111u << j;
+        c4 |= static_cast<uint32_t>(__popc(b0 & mj) + __popc(b1 & mj)) << (8 * j);
+      }
+      cnt4[it] = c4;
+      nzz[it] = static_cast<uint32_t>(__popc(b0) + __popc(b1)) |
+                (static_cast<uint32_t>(__popc(z0) + __popc(z1)) << 16);
+    }
+  }
+  __syncthreads();
+
+  // ---- prefixes: per bank over its items (warp 0), scan order over all items (warp 1)
+  if (warp == 0) {
+    const int x0 = lane >> 2, j = lane & 3;
+    uint32_t run = 0;
+    for (int x = x0; x < m_tb; x += 8) {
+      for (int ch = 0; ch < nch; ++ch) {
+        const int it = x * nch + ch;
+        bpre[it * 4 + j] = static_cast<uint16_t>(run);
+        run += (cnt4[it] >> (8 * j)) & 0xFFu;
+      }
+    }
+    cb[lane] = run;
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, run);
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, run);
+    if (lane == 0) {
+      cb[32] = tot;
+      cb[33] = mx;
+    }
+  } else if (warp == 1) {
+    uint32_t carry_n = 0, carry_z = 0;
+    for (int base = 0; base < lay.items; base += 32) {
+      const int it = base + lane;
+      const uint32_t v = it < lay.items ? nzz[it] : 0u;
+      uint32_t n = v & 0xFFFFu, z = v >> 16;
+      uint32_t in = n, iz = z;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t tn = __shfl_up_sync(0xffffffffu, in, d), tz = __shfl_up_sync(0xffffffffu, iz, d);
+        if (lane >= d) {
+          in += tn;
+          iz += tz;
+        }
+      }
+      if (it < lay.items) {
+        npre[it] = carry_n + in - n;
+        zpre[it] = carry_z + iz - z;
+      }
+      carry_n += __shfl_sync(0xffffffffu, in, 31);
+      carry_z += __shfl_sync(0xffffffffu, iz, 31);
+    }
+  }
+  __syncthreads();
+
+  const uint32_t nnz = cb[32];
+  const uint32_t maxc = cb[33];
+  const uint32_t pad = (32u - (nnz & 31u)) & 31u;
+  const uint32_t base = offsets[tile];
+  if (offsets[tile + 1] - base != nnz + pad) {  // count pass / offsets disagree
+    if (threadIdx.x == 0) raise_dev(err, TCSL_STATUS_INCONSISTENT_OFFSETS);
+    return;
+  }
+  if (reorder) {
+    for (uint32_t L = threadIdx.x + 1; L <= maxc; L += blockDim.x) {
+      uint32_t f = 0, mask = 0;
+#pragma unroll 8
+      for (int b = 0; b < 32; ++b) {
+        const uint32_t c = cb[b];
+        f += c > L ? c - L : 0u;
+        mask |= static_cast<uint32_t>(c >= L) << b;
+      }
+      fl[L] = f;
+      ml[L] = mask;
+    }
+    __syncthreads();
+  }
+
+  // ---- pass B: place every nonzero and the first `pad` zero positions
+  uint32_t* out = lay.stage ? stg : entries + base;
+  for (int it = warp; it < lay.items; it += nwarps) {
+    const int x = it / nch, ch = it - x * nch;
+    const int y0 = ch * 64 + 2 * lane;
+    const Pair p = load_pair(w, k, r0, c0, x, y0, x_end, y_end, k_tb);
+    const uint32_t b0 = __ballot_sync(0xffffffffu, p.nz0), b1 = __ballot_sync(0xffffffffu, p.nz1);
+    const bool zp0 = p.in0 && !p.nz0, zp1 = p.in1 && !p.nz1;
+    const uint32_t z0 = __ballot_sync(0xffffffffu, zp0), z1 = __ballot_sync(0xffffffffu, zp1);
+    const uint32_t loc0 = static_cast<uint32_t>(x * k_tb + y0);
+    if (p.nz0 || p.nz1) {
+      uint32_t pos0, pos1;
+      if (reorder) {
+        const int j = lane & 3;
+        const uint32_t mj = 0x11111111u << j;
+        const int b = (x & 7) * 4 + j;
+        const uint32_t kb = bpre[it * 4 + j] + __popc(b0 & mj & lt) + __popc(b1 & mj & lt);
+        const uint32_t c = cb[b];
+        const uint32_t below = (1u << b) - 1u;
+        const uint32_t L0 = c - kb;
+        pos0 = fl[L0] + __popc(ml[L0] & below);
+        const uint32_t L1 = c - kb - (p.nz0 ? 1u : 0u);
+        pos1 = fl[L1] + __popc(ml[L1] & below);
+      } else {
+        pos0 = npre[it] + __popc(b0 & lt) + __popc(b1 & lt);
+        pos1 = pos0 + (p.nz0 ? 1u : 0u);
+      }
+      if (p.nz0) out[pos0] = (p.v0 << 16) | loc0;
+      if (p.nz1) out[pos1] = (p.v1 << 16) | (loc0 + 1);
+    }
+    if (pad && (zp0 || zp1)) {
+      const uint32_t zr0 = zpre[it] + __popc(z0 & lt) + __popc(z1 & lt);
+      const uint32_t zr1 = zr0 + (zp0 ? 1u : 0u);
+      if (zp0 && zr0 < pad) out[nnz + zr0] = loc0;
+      if (zp1 && zr1 < pad) out[nnz + zr1] = loc0 + 1;
+    }
+  }
+  if (lay.stage) {
+    __syncthreads();
+    const uint32_t total = nnz + pad;  // multiple of 32, base multiple of 32: 128-B aligned spans
+    uint4* dst = reinterpret_cast<uint4*>(entries + base);
+    const uint4* src = reinterpret_cast<const uint4*>(stg);
+    for (uint32_t i = threadIdx.x; i < total / 4; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_encode_count(const uint16_t* w, uint32_t m, uint32_t k, int m_tb, int k_tb,
+                                uint32_t* counts, cudaStream_t s) {
+  const int tk = div_up_i(k, k_tb);
+  const long long tiles = static_cast<long long>(div_up_i(m, m_tb)) * tk;
+  if (tiles > 0) encode_count_kernel<<<static_cast<unsigned>(tiles), 256, 0, s>>>(w, m, k, m_tb, k_tb, tk, counts);
+  return cudaGetLastError();
+}
+
+size_t encode_scan_temp_bytes(uint32_t tiles) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                static_cast<int>(tiles) + 1);
+  return bytes;
+}
+
+cudaError_t launch_encode_scan(uint32_t* counts_in, uint32_t* offsets, uint32_t tiles, void* temp,
+                               size_t temp_bytes, cudaStream_t s) {
+  return cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts_in, offsets, static_cast<int>(tiles) + 1, s);
+}
+
+cudaError_t launch_encode_emit(const uint16_t* w, uint32_t m, uint32_t k, int m_tb, int k_tb, int reorder,
+                               const uint32_t* offsets, uint32_t* entries, int* err, cudaStream_t s) {
+  const int tk = div_up_i(k, k_tb);
+  const long long tiles = static_cast<long long>(div_up_i(m, m_tb)) * tk;
+  const EmitLayout lay = emit_layout(m_tb, k_tb);
+  cudaError_t e = cudaFuncSetAttribute(encode_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(lay.bytes));
+  if (e != cudaSuccess) return e;
+  if (tiles > 0)
+    encode_emit_kernel<<<static_cast<unsigned>(tiles), 256, lay.bytes, s>>>(w, m, k, m_tb, k_tb, tk, reorder,
+                                                                           offsets, entries, err);
+  return cudaGetLastError();
+}
+
+}  // namespace tcslk

@@ -1,0 +1,155 @@
+"""GPU encoder / decoder parity: bit-exact against the CPU oracle and the
+reference's golden artifacts (proj/tests/acceptance.cpp:60-64, test_codec.cpp)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).cuda()
+
+
+def _gpu_encode(a, m_tb=128, k_tb=64, reorder=True):
+    import paper_2309_10285_b200 as tc
+    return tc.encode(_dev(a), tc.TileConfig(m_tb, k_tb), reorder)
+
+
+def _same(port, a, m_tb=128, k_tb=64, reorder=True):
+    t = _gpu_encode(a, m_tb, k_tb, reorder)
+    off, ent = t.to_host()
+    want = port.encode(a, m_tb, k_tb, reorder)
+    assert off.shape == want.offsets.shape and (off == want.offsets).all()
+    assert ent.shape == want.entries.shape
+    bad = np.nonzero(ent != want.entries)[0]
+    assert bad.size == 0, f"first mismatch at {bad[:5]}: {ent[bad[:5]]} vs {want.entries[bad[:5]]}"
+    return t, want
+
+
+GOLDEN = [("golden_a.tcsl", 128, 64, 0.3, 11, True, 0xa57f18792a5f0447),
+          ("golden_b.tcsl", 256, 128, 0.8, 22, True, 0x2a290613b42e2457),
+          ("golden_c.tcsl", 130, 70, 0.5, 33, False, 0xf68ef9afd7dea93a)]
+
+
+@pytest.mark.parametrize("g", GOLDEN, ids=[g[0] for g in GOLDEN])
+def test_golden_artifacts(port, g):
+    from oracle import Tcsl
+    name, r, c, beta, seed, reorder, want_hash = g
+    a = port.gen_random_sparse(r, c, beta, seed)
+    t = _gpu_encode(a, reorder=reorder)
+    off, ent = t.to_host()
+    data = port.serialize(Tcsl(r, c, 128, 64, reorder, off, ent))
+    assert port.fnv1a(data) == want_hash
+    with open(os.path.join(GOLD, name), "rb") as f:
+        assert f.read() == data
+
+
+def test_kat_fixture(port):
+    from oracle import Tcsl
+    with open(os.path.join(GOLD, "kats.json")) as f:
+        kats = json.load(f)["encode"]
+    for c in kats:
+        a = port.gen_random_sparse(c["rows"], c["cols"], c["beta"], c["seed"])
+        t = _gpu_encode(a, c["m_tb"], c["k_tb"], c["reorder"])
+        off, ent = t.to_host()
+        data = port.serialize(Tcsl(c["rows"], c["cols"], c["m_tb"], c["k_tb"], c["reorder"], off, ent))
+        assert hex(port.fnv1a(data)) == c["fnv"], c
+
+
+def test_worked_example_and_greedy_order(port):  # test_codec.cpp:48-84
+    a = np.zeros((128, 64), np.uint16)
+    a[0, 0], a[1, 2] = 0x3C00, 0x4000
+    t, _ = _same(port, a)
+    _, ent = t.to_host()
+    assert ent[0] == 0x3C000000 and ent[1] == 0x40000042
+    b = np.zeros((128, 64), np.uint16)
+    b[0, 0], b[1, 0], b[1, 1] = 0x3C00, 0x4000, 0x4200
+    t, _ = _same(port, b)
+    assert [int(e) & 0xFFFF for e in t.to_host()[1][:3]] == [64, 0, 65]
+    _same(port, b, reorder=False)
+    _same(port, np.zeros((128, 64), np.uint16))
+
+
+@pytest.mark.parametrize("cfg", [(128, 64), (16, 8), (256, 64), (64, 32), (8, 512), (512, 8), (64, 1024)])
+def test_fuzz_tile_configs(port, cfg):
+    rng = np.random.default_rng(hash(cfg) & 0xFFFF)
+    for it in range(6):
+        m, k = int(rng.integers(1, 700)), int(rng.integers(1, 700))
+        beta = float(rng.choice([0.0, 0.3, 0.5, 0.7, 0.8, 0.9, 0.99, 1.0]))
+        a = port.gen_random_sparse(m, k, beta, int(rng.integers(0, 2**62)))
+        _same(port, a, cfg[0], cfg[1], it % 2 == 0)
+
+
+def test_special_bit_patterns(port):
+    rng = np.random.default_rng(5)
+    a = rng.integers(0, 65536, size=(300, 190), dtype=np.uint32).astype(np.uint16)
+    a[rng.random(a.shape) < 0.6] = 0
+    specials = np.array([0x8000, 0x7C00, 0xFC00, 0x7E00, 0x7C01, 0x0001, 0x83FF, 0x03FF], np.uint16)
+    idx = rng.integers(0, a.size, 2000)
+    a.reshape(-1)[idx] = specials[rng.integers(0, len(specials), 2000)]
+    for reorder in (True, False):
+        _same(port, a, reorder=reorder)
+        _same(port, a, 16, 8, reorder)
+
+
+def test_c1_full_size_bit_exact(port):  # config 0 shape: 7168 x 7168 at 80 %
+    import paper_2309_10285_b200 as tc
+    a = port.gen_random_sparse(7168, 7168, 0.8, 1)
+    t, want = _same(port, a)
+    assert t.n_entries == 10374432  # SURVEY.md Appendix A.6 (seed 1)
+    assert port.reg_pressure(want) == 14
+
+
+def test_decode_round_trip_full_size():
+    """encode -> decode is the identity (up to -0 -> +0) at a BASELINE shape."""
+    import torch
+
+    import paper_2309_10285_b200 as tc
+    w = tc.gen_synthetic(9216, 36864, 0.9, 7)
+    w.view(-1)[::1001] = -32768  # -0.0 folds to +0.0
+    t = tc.encode(w)
+    d = tc.decode(t)
+    want = torch.where((w & 0x7FFF) == 0, torch.zeros_like(w), w)
+    assert torch.equal(d, want)
+    assert all(int(x) % 32 == 0 for x in torch.diff(t.offsets.long()).unique().tolist())
+
+
+def test_decode_errors(port):
+    import paper_2309_10285_b200 as tc
+    a = np.zeros((128, 64), np.uint16)
+    a[0, 0] = 0x3C00
+    t = _gpu_encode(a)
+    t.entries[1] = 8192
+    with pytest.raises(tc.TcslError, match="location_out_of_range"):
+        tc.decode(t)
+    f = port.gen_random_sparse(100, 64, 0.501, 3)
+    tf = _gpu_encode(f)
+    off, ent = tf.to_host()
+    i = int(np.nonzero((ent >> 16) == 0)[0][0])
+    tf.entries[i] = int(np.int32(np.uint32((0x3C00 << 16) | (110 * 64)).view(np.int32)))
+    with pytest.raises(tc.TcslError, match="location_out_of_range"):
+        tc.decode(tf)
+    t2 = _gpu_encode(a)
+    t2.offsets[1] = 16
+    with pytest.raises(tc.TcslError, match="inconsistent_offsets"):
+        tc.validate(t2)
+
+
+def test_shard_slices_equal_reencoding(port):
+    import paper_2309_10285_b200 as tc
+    a = port.gen_random_sparse(1000, 700, 0.8, 11)
+    t = _gpu_encode(a)
+    for g in (2, 3, 4):
+        tm = t.tiles_m
+        bounds = [tm * i // g for i in range(g + 1)]
+        for tr0, tr1 in zip(bounds[:-1], bounds[1:]):
+            sh = tc.shard_rows(t, tr0, tr1)
+            off, ent = sh.to_host()
+            want = port.encode(a[tr0 * 128:min(1000, tr1 * 128)])
+            assert (off == want.offsets).all() and (ent == want.entries).all()
