@@ -2,6 +2,9 @@
 // reference's error classes, workspace carving, and kernel dispatch.
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "tcsl_internal.cuh"
 
@@ -38,7 +41,16 @@ int x_pitch(int n) { return (n + 7) / 8 * 8; }
 int effective_split(uint32_t m, uint32_t k, int n, int split_k) {
   const int tiles_k = tcslk::div_up_i(k, 64);
   if (split_k > 0) return split_k < tiles_k ? split_k : tiles_k;
-  return tcslk::auto_split(m, k, n, 0.2 * 8192);
+  // the heuristic simulates the persistent schedule; memoise it per shape
+  static std::mutex mu;
+  static std::map<std::tuple<uint32_t, uint32_t, int>, int> cache;
+  const auto key = std::make_tuple(m, k, n);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int s = tcslk::auto_split(m, k, n, 0.2 * 8192);
+  cache.emplace(key, s);
+  return s;
 }
 
 struct SpmmWs {

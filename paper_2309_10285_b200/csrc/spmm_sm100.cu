@@ -9,14 +9,15 @@
 // bit-exact CUDA-core mode.
 //
 // One persistent CTA per SM, warp-specialised (512 threads):
-//   warp 0      entry producer: streams the unit's contiguous entry span
-//               [off[t0], off[t1]) with cp.async.bulk into a ring of 4 KB chunks
-//   warp 1      X producer: TMA-loads the 64 x n_pad activation tile per k-tile
-//               (MN-major, hardware swizzle = 2*n_pad bytes)
-//   warp 2      TMEM owner + single-thread tcgen05.mma issuer (M=128, N=n_pad, K=16 x 4)
+//   warp 0      entry producer: streams each unit's contiguous entry span
+//               [off[t0], off[t1]) with cp.async.bulk into a ring of 2 KB chunks
+//   warp 1      X producer: TMA-loads the 64 x NPAD activation tile per k-tile
+//               (MN-major, hardware swizzle = 2*NPAD bytes)
+//   warp 2      TMEM owner + single-thread tcgen05.mma issuer (M=128, N=NPAD, K=16 x 4)
 //   warps 4-7   epilogue: tcgen05.ld accumulator -> fp32 Y rows (or split-K partials)
-//   warps 8-15  decode: scatter each 32-entry group (one entry per lane) into the
-//               dense tile in the SWIZZLE_NONE K-major core-matrix layout
+//   warps 8-15  decode, two teams of 4 warps working on alternate k-tiles: zero
+//               the dense tile, then scatter each 32-entry group (one entry per
+//               lane) into the SWIZZLE_NONE K-major core-matrix layout
 // The core-matrix layout puts element (x, y) in bank (x%8)*4 + (y%8)/2, which is
 // exactly the reference's bank_id (proj/include/tcsl/tcsl_format.hpp:18), so the
 // encoder's ahead-of-time bank reordering keeps the scatter near one wavefront
@@ -39,12 +40,37 @@ namespace tcslk {
 namespace {
 
 constexpr int kMTB = 128, kKTB = 64;
-constexpr int kABytes = kMTB * kKTB * 2;  // dense fp16 tile, 16 KB
-constexpr int kNA = 3;                    // dense-tile buffers
-constexpr int kNDec = 8;                  // decode warps
-constexpr int kChunk = 1024;              // entries per ring chunk (4 KB)
+constexpr uint32_t kABytes = kMTB * kKTB * 2;  // dense fp16 tile, 16 KB
+constexpr int kNA = 4;                         // dense-tile buffers (2 per decode team)
+constexpr int kTeamWarps = 4;                  // warps per decode team
+constexpr uint32_t kChunk = 512;               // entries per ring chunk (2 KB); chunks are tile-aligned
+constexpr uint32_t kRingT = 20;                // chunks per team ring (40 KB; >= one dense tile + slack)
 constexpr int kThreads = 512;
 constexpr int kWarpEpi = 4, kWarpDec = 8;
+
+template <int NPAD>
+struct Cfg {
+  static constexpr int kBoxW = NPAD < 64 ? NPAD : 64;       // TMA box / swizzle atom width
+  static constexpr int kBoxes = NPAD / kBoxW;
+  static constexpr uint32_t kBoxBytes = 64u * kBoxW * 2;    // 64 k-rows
+  static constexpr uint32_t kXStage = kBoxBytes * kBoxes;
+  static constexpr int kNX = (32768 / kXStage) < 2 ? 2 : ((32768 / kXStage) > 8 ? 8 : (32768 / kXStage));
+  static constexpr uint32_t kRowBytes = kBoxW * 2;
+  static constexpr uint32_t kLayout = kRowBytes == 16 ? 0u : (kRowBytes == 32 ? 6u : (kRowBytes == 64 ? 4u : 2u));
+  // SWIZZLE_NONE (NPAD=8): LBO = k-group stride (8 rows x 16 B); swizzled: SBO = 8-row
+  // k-group stride, LBO = stride between 64-column atoms.
+  static constexpr uint32_t kLBO = kRowBytes == 16 ? 128u : kBoxBytes;
+  static constexpr uint32_t kSBO = kRowBytes == 16 ? 128u : 8u * kRowBytes;
+  static constexpr uint32_t kKStep = 16u * kRowBytes;       // 16 k-rows per MMA
+  static constexpr uint32_t kTmemCols = (2 * NPAD) <= 32 ? 32 : ((2 * NPAD) <= 64 ? 64 : ((2 * NPAD) <= 128 ? 128 : ((2 * NPAD) <= 256 ? 256 : 512)));
+  static constexpr uint32_t kIdesc = idesc_f16_f32(128, NPAD, 1);
+  // smem carve-up (from a 1024-aligned base)
+  static constexpr uint32_t kOffX = kNA * kABytes;
+  static constexpr uint32_t kOffE = kOffX + kNX * kXStage;
+  static constexpr uint32_t kOffBar = kOffE + 2 * kRingT * kChunk * 4;
+  static constexpr uint32_t kNumBars = 2 * kNA + 2 * kNX + 4 * kRingT + 4;
+  static constexpr uint32_t kSmem = 1024 + kOffBar + 8 * kNumBars + 16;
+};
 
 struct Params {
   const uint32_t* off;
@@ -52,31 +78,19 @@ struct Params {
   uint64_t n_entries;
   uint32_t m, k;
   int tiles_m, tiles_k;
-  int n, n_pad, col0, split, units;
+  int n, col0, split, units;
   float* out;
   int ldo;
   int* err;
-  int nx, ring;
-  uint32_t x_stage, x_box_bytes;
-  int x_boxes, box_w;
-  uint32_t tmem_cols, idesc, b_layout, b_lbo, b_sbo, b_kstep;
+  unsigned long long* trace;  // TCSL_TRACE builds only: per-event clock64 stamps of CTA 0
 };
 
-struct Bars {
-  uint32_t base;
-  int nx, ring;
-  __device__ uint32_t afull(int i) const { return base + 8 * i; }
-  __device__ uint32_t aempty(int i) const { return base + 8 * (kNA + i); }
-  __device__ uint32_t xfull(int i) const { return base + 8 * (2 * kNA + i); }
-  __device__ uint32_t xempty(int i) const { return base + 8 * (2 * kNA + nx + i); }
-  __device__ uint32_t efull(int i) const { return base + 8 * (2 * kNA + 2 * nx + i); }
-  __device__ uint32_t eempty(int i) const { return base + 8 * (2 * kNA + 2 * nx + ring + i); }
-  __device__ uint32_t dfull(int i) const { return base + 8 * (2 * kNA + 2 * nx + 2 * ring + i); }
-  __device__ uint32_t dempty(int i) const { return base + 8 * (2 * kNA + 2 * nx + 2 * ring + 2 + i); }
-  __device__ uint32_t count() const { return 2 * kNA + 2 * nx + 2 * ring + 4; }
-};
-
-__host__ __device__ inline size_t bar_bytes(int nx, int ring) { return 8ull * (2 * kNA + 2 * nx + 2 * ring + 4) + 16; }
+#ifdef TCSL_TRACE
+#define TRACE(slot, idx) \
+  do { if (blockIdx.x == 0 && p.trace && (idx) < 4096) p.trace[(slot) * 4096 + (idx)] = clock64(); } while (0)
+#else
+#define TRACE(slot, idx) do { } while (0)
+#endif
 
 struct Unit {
   int rb, s, kt0, kt1;
@@ -101,80 +115,100 @@ __device__ __forceinline__ bool unit_span(const Params& p, const Unit& u, uint32
   }
   return true;
 }
+// A tile's span is streamed / decoded only when it sits inside the unit span
+// as whole 32-entry groups; producer and decoders apply the same rule.
+__device__ __forceinline__ uint32_t tile_groups(uint32_t e0, uint32_t e1, uint32_t a0, uint32_t a1) {
+  return (e0 <= a0 && a0 <= a1 && a1 <= e1 && ((a1 - a0) & 31u) == 0) ? (a1 - a0) >> 5 : 0u;
+}
 
 // Byte offset of tile element `loc` (= x*64 + y) in the K-major SWIZZLE_NONE
-// canonical layout: (x/8)*1024 + (y/8)*128 + (x%8)*16 + (y%8)*2.
+// canonical layout: (x/8)*1024 + (y/8)*128 + (x%8)*16 + (y%8)*2. Bits >= 13 of
+// loc are ignored, so the address is always inside the 16 KB tile.
 __device__ __forceinline__ uint32_t a_offset(uint32_t loc) {
-  return ((loc << 1) & 0x3C0Eu)      // (y%8)*2 from loc[2:0], (x/8)*1024 from loc[12:9]
-         | ((loc >> 2) & 0x70u)      // (x%8)*16 from loc[8:6]
-         | ((loc << 4) & 0x380u);    // (y/8)*128 from loc[5:3]
+  return ((loc << 1) & 0x3C0Eu)  // (y%8)*2 from loc[2:0], (x/8)*1024 from loc[12:9]
+         | ((loc >> 2) & 0x70u)  // (x%8)*16 from loc[8:6]
+         | ((loc << 4) & 0x380u);  // (y/8)*128 from loc[5:3]
 }
 
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
+template <int NPAD>
 __global__ void __launch_bounds__(kThreads, 1)
     spmm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t s_a = smem_u32(smem);
-  const uint32_t s_x = s_a + kNA * kABytes;
-  const uint32_t s_e = s_x + p.nx * p.x_stage;
-  const uint32_t* ring_e = reinterpret_cast<const uint32_t*>(smem + (s_e - s_a));
-  Bars bars{s_e + static_cast<uint32_t>(p.ring) * kChunk * 4, p.nx, p.ring};
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + (bars.base - s_a) + 8 * bars.count());
+  using C = Cfg<NPAD>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t s_a = (raw + 1023u) & ~1023u;
+  const uint32_t s_x = s_a + C::kOffX;
+  const uint32_t s_e = s_a + C::kOffE;  // team t ring at s_e + t * kRingT * kChunk * 4
+  const uint32_t s_bar = s_a + C::kOffBar;
+  const uint32_t b_afull = s_bar, b_aempty = s_bar + 8 * kNA;
+  const uint32_t b_xfull = s_bar + 8 * (2 * kNA), b_xempty = b_xfull + 8 * C::kNX;
+  const uint32_t b_efull = b_xempty + 8 * C::kNX;  // [team][kRingT]
+  const uint32_t b_eempty = b_efull + 8 * 2 * kRingT;
+  const uint32_t b_dfull = b_eempty + 8 * 2 * kRingT, b_dempty = b_dfull + 16;
+  const uint32_t s_tmem_slot = b_dempty + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (s_tmem_slot - raw));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNA; ++i) {
-      mbar_init(bars.afull(i), kNDec);
-      mbar_init(bars.aempty(i), 1);
+      mbar_init(b_afull + 8 * i, kTeamWarps);
+      mbar_init(b_aempty + 8 * i, 1);
     }
-    for (int i = 0; i < p.nx; ++i) {
-      mbar_init(bars.xfull(i), 1);
-      mbar_init(bars.xempty(i), 1);
+    for (int i = 0; i < C::kNX; ++i) {
+      mbar_init(b_xfull + 8 * i, 1);
+      mbar_init(b_xempty + 8 * i, 1);
     }
-    for (int i = 0; i < p.ring; ++i) {
-      mbar_init(bars.efull(i), 1);
-      mbar_init(bars.eempty(i), kNDec);
+    for (uint32_t i = 0; i < 2 * kRingT; ++i) {
+      mbar_init(b_efull + 8 * i, 1);
+      mbar_init(b_eempty + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(bars.dfull(i), 1);
-      mbar_init(bars.dempty(i), 4);
+      mbar_init(b_dfull + 8 * i, 1);
+      mbar_init(b_dempty + 8 * i, 4);
     }
     fence_barrier_init();
   }
   if (warp == 1 && lane == 0) prefetch_tmap(&tmap_x);
-  if (warp == 2) tmem_alloc_dyn(smem_u32(tmem_slot), p.tmem_cols);
-  {  // dense tiles start as +0.0 everywhere
-    uint4* a4 = reinterpret_cast<uint4*>(smem);
-    for (int i = threadIdx.x; i < kNA * kABytes / 16; i += kThreads) a4[i] = make_uint4(0, 0, 0, 0);
-  }
+  if (warp == 2) tmem_alloc_dyn(s_tmem_slot, C::kTmemCols);
+  for (uint32_t i = threadIdx.x; i < kNA * kABytes / 16; i += kThreads) sts128_zero(s_a + 16 * i);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ---------------------------------------------------------------- entry producer
+  if (warp == 0 || warp == 3) {
+    // ------------------------------------------------------ entry producers (one per team)
+    // Streams the entry span of every k-tile of its team (gt % 2 == team) into
+    // the team ring, in tile-aligned 2 KB chunks.
     if (lane == 0) {
+      const uint32_t team = warp == 0 ? 0u : 1u;
+      const uint32_t ring = s_e + team * kRingT * kChunk * 4;
+      const uint32_t efull = b_efull + 8 * team * kRingT, eempty = b_eempty + 8 * team * kRingT;
       const uint64_t pol = policy_evict_first();
-      uint32_t g = 0;
+      uint32_t g = 0, gt = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const Unit un = unit_of(p, u);
         uint32_t e0, e1;
-        if (!unit_span(p, un, e0, e1)) raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
-        for (uint32_t c0 = e0; c0 < e1; c0 += kChunk, ++g) {
-          const int slot = static_cast<int>(g % p.ring);
-          const uint32_t use = g / p.ring;
-          if (use > 0) mbar_wait(bars.eempty(slot), (use - 1) & 1);
-          const uint32_t bytes = min(static_cast<uint32_t>(kChunk), e1 - c0) * 4;
-          mbar_arrive_expect_tx(bars.efull(slot), bytes);
-          bulk_g2s(s_e + slot * kChunk * 4, p.ent + c0, bytes, bars.efull(slot), pol);
+        if (!unit_span(p, un, e0, e1) && team == 0) raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
+        const uint32_t tile0 = static_cast<uint32_t>(un.rb) * p.tiles_k + un.kt0;
+        for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
+          if ((gt & 1u) != team) continue;
+          const uint32_t t = tile0 + (kt - un.kt0);
+          const uint32_t a0 = __ldg(p.off + t), a1 = __ldg(p.off + t + 1);
+          const uint32_t ng = tile_groups(e0, e1, a0, a1);
+          for (uint32_t c0 = 0; c0 < 32 * ng; c0 += kChunk, ++g) {
+            const uint32_t slot = g % kRingT;
+            const uint32_t use = g / kRingT;
+            if (team == 0) TRACE(9, g);
+            if (use > 0) mbar_wait_sleep(eempty + 8 * slot, (use - 1) & 1);
+            if (team == 0) TRACE(10, g);
+            const uint32_t bytes = min(kChunk, 32 * ng - c0) * 4;
+            mbar_arrive_expect_tx(efull + 8 * slot, bytes);
+            bulk_g2s(ring + slot * kChunk * 4, p.ent + a0 + c0, bytes, efull + 8 * slot, pol);
+          }
         }
       }
     }
@@ -186,13 +220,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const Unit un = unit_of(p, u);
         for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
-          const int slot = static_cast<int>(gt % p.nx);
-          const uint32_t use = gt / p.nx;
-          if (use > 0) mbar_wait(bars.xempty(slot), (use - 1) & 1);
-          mbar_arrive_expect_tx(bars.xfull(slot), p.x_stage);
-          for (int bx = 0; bx < p.x_boxes; ++bx)
-            tma_load_2d(s_x + slot * p.x_stage + bx * p.x_box_bytes, &tmap_x, p.col0 + bx * p.box_w, kt * kKTB,
-                        bars.xfull(slot), pol);
+          const uint32_t slot = gt % C::kNX;
+          const uint32_t use = gt / C::kNX;
+          if (use > 0) mbar_wait_sleep(b_xempty + 8 * slot, (use - 1) & 1);
+          mbar_arrive_expect_tx(b_xfull + 8 * slot, C::kXStage);
+#pragma unroll
+          for (int bx = 0; bx < C::kBoxes; ++bx)
+            tma_load_2d(s_x + slot * C::kXStage + bx * C::kBoxBytes, &tmap_x, p.col0 + bx * C::kBoxW, kt * kKTB,
+                        b_xfull + 8 * slot, pol);
         }
       }
     }
@@ -202,28 +237,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t gt = 0, ui = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
         const Unit un = unit_of(p, u);
-        const int acc = static_cast<int>(ui & 1);
-        if (ui >= 2) mbar_wait(bars.dempty(acc), ((ui >> 1) - 1) & 1);
+        const uint32_t acc = ui & 1;
+        if (ui >= 2) mbar_wait_sleep(b_dempty + 8 * acc, ((ui >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem + static_cast<uint32_t>(acc * p.n_pad);
+        const uint32_t d_tmem = tmem + acc * NPAD;
         for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
-          const int b = static_cast<int>(gt % kNA);
-          const int xs = static_cast<int>(gt % p.nx);
-          mbar_wait(bars.afull(b), (gt / kNA) & 1);
-          mbar_wait(bars.xfull(xs), (gt / p.nx) & 1);
+          const uint32_t b = gt % kNA;
+          const uint32_t xs = gt % C::kNX;
+          TRACE(5, gt);
+          mbar_wait(b_afull + 8 * b, (gt / kNA) & 1);
+          TRACE(6, gt);
+          mbar_wait(b_xfull + 8 * xs, (gt / C::kNX) & 1);
+          TRACE(7, gt);
           tc_fence_after();
           const uint32_t a0 = s_a + b * kABytes;
-          const uint32_t b0 = s_x + xs * p.x_stage;
+          const uint32_t x0 = s_x + xs * C::kXStage;
 #pragma unroll
           for (int s = 0; s < kKTB / 16; ++s) {
             const uint64_t ad = smem_desc(a0 + s * 256, 128, 1024, 0);
-            const uint64_t bd = smem_desc(b0 + s * p.b_kstep, p.b_lbo, p.b_sbo, p.b_layout);
-            mma_f16_ss(d_tmem, ad, bd, p.idesc, (kt > un.kt0 || s > 0) ? 1u : 0u);
+            const uint64_t bd = smem_desc(x0 + s * C::kKStep, C::kLBO, C::kSBO, C::kLayout);
+            mma_f16_ss(d_tmem, ad, bd, C::kIdesc, (kt > un.kt0 || s > 0) ? 1u : 0u);
           }
-          mma_commit(bars.aempty(b));
-          mma_commit(bars.xempty(xs));
+          mma_commit(b_aempty + 8 * b);
+          mma_commit(b_xempty + 8 * xs);
+#ifdef TCSL_TRACE
+          if (blockIdx.x == 0 && p.trace) {  // debug only: measure MMA completion latency
+            mbar_wait(b_aempty + 8 * b, (gt / kNA) & 1);
+            TRACE(8, gt);
+          }
+#endif
         }
-        mma_commit(bars.dfull(acc));
+        mma_commit(b_dfull + 8 * acc);
       }
     }
     __syncwarp();
@@ -233,25 +277,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ui = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
       const Unit un = unit_of(p, u);
-      const int acc = static_cast<int>(ui & 1);
-      mbar_wait(bars.dfull(acc), (ui >> 1) & 1);
+      const uint32_t acc = ui & 1;
+      mbar_wait_sleep(b_dfull + 8 * acc, (ui >> 1) & 1);
       tc_fence_after();
       const long long row = static_cast<long long>(un.rb) * kMTB + q * 32 + lane;
       float* dst = p.out + (p.split > 1 ? static_cast<long long>(un.s) * p.m * p.ldo : 0ll) + row * p.ldo + p.col0;
       const bool row_ok = row < p.m;
-      const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * p.n_pad);
-      const int ncol = min(p.n_pad, p.n - p.col0);
-      if (p.n_pad == 8) {
+      const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * NPAD;
+      const int ncol = min(NPAD, p.n - p.col0);
+      if constexpr (NPAD == 8) {
         uint32_t r[8];
         tmem_ld8(t_base, r);
         tmem_ld_wait();
         if (row_ok) {
+          if (ncol == 8 && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
+            reinterpret_cast<float4*>(dst)[0] =
+                make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3]));
+            reinterpret_cast<float4*>(dst)[1] =
+                make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7]));
+          } else {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (j < ncol) dst[j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 8; ++j)
+              if (j < ncol) dst[j] = __uint_as_float(r[j]);
+          }
         }
       } else {
-        for (int c0 = 0; c0 < p.n_pad; c0 += 16) {
+#pragma unroll
+        for (int c0 = 0; c0 < NPAD; c0 += 16) {
           uint32_t r[16];
           tmem_ld16(t_base + c0, r);
           tmem_ld_wait();
@@ -272,83 +324,132 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bars.dempty(acc));
+      if (lane == 0) mbar_arrive(b_dempty + 8 * acc);
     }
   } else if (warp >= kWarpDec) {
     // ---------------------------------------------------------------- decode
+    // Team t (4 warps) decodes the k-tiles with gt % 2 == t into buffers t, t+2.
     const int dw = warp - kWarpDec;
+    const uint32_t team = dw / kTeamWarps;
+    const int tw = dw % kTeamWarps;
+    const uint32_t ring = s_e + team * kRingT * kChunk * 4;
+    const uint32_t efull = b_efull + 8 * team * kRingT, eempty = b_eempty + 8 * team * kRingT;
     uint32_t gt = 0;
-    uint32_t g_base = 0;  // first ring chunk of the current unit
-    uint32_t nxt = 0;     // chunks < nxt have been waited full
-    uint32_t rel = 0;     // chunks < rel have been released
+    uint32_t cbase = 0;                   // first team-ring chunk of the current tile
+    uint32_t prev_base = 0, prev_n = 0;   // chunks of this team's previous tile (released after the barrier)
+    uint32_t nxt = 0;                     // team-ring chunks < nxt have been waited full by this warp
+    uint32_t err_or = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const Unit un = unit_of(p, u);
       uint32_t e0, e1;
       unit_span(p, un, e0, e1);
-      const uint32_t nchunks = (e1 - e0 + kChunk - 1) / kChunk;
-      for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
-        const int b = static_cast<int>(gt % kNA);
+      const uint32_t tile0 = static_cast<uint32_t>(un.rb) * p.tiles_k + un.kt0;
+      const int ntiles = un.kt1 - un.kt0;
+      // offsets window: lane l holds off[tile0 + 32*w + l]
+      const uint32_t last_off = tile0 + ntiles;
+      uint32_t win_cur = __ldg(p.off + min(tile0 + lane, last_off));
+      uint32_t win_nxt = __ldg(p.off + min(tile0 + 32 + lane, last_off));
+      int win = 0;
+      for (int i = 0; i < ntiles; ++i, ++gt) {
+        if ((i >> 5) != win) {  // slide the window by 32 tiles
+          win_cur = win_nxt;
+          ++win;
+          win_nxt = __ldg(p.off + min(tile0 + 32 * (win + 1) + lane, last_off));
+        }
+        if ((gt & 1u) != team) continue;
+        const uint32_t a0 = __shfl_sync(0xffffffffu, win_cur, i & 31);
+        const uint32_t a1n = __shfl_sync(0xffffffffu, win_nxt, 0);
+        const uint32_t a1c = __shfl_sync(0xffffffffu, win_cur, (i + 1) & 31);
+        const uint32_t a1 = ((i & 31) == 31) ? a1n : a1c;
+        const uint32_t ng = tile_groups(e0, e1, a0, a1);
+        const uint32_t b = gt % kNA;
         const uint32_t use = gt / kNA;
-        uint8_t* a_tile = smem + b * kABytes;
+        const uint32_t a_tile = s_a + b * kABytes;
+        if (tw == 0 && lane == 0) TRACE(0, gt);
         if (use > 0) {
-          mbar_wait(bars.aempty(b), (use - 1) & 1);
-          uint4* a4 = reinterpret_cast<uint4*>(a_tile);
-          for (int i = dw * 32 + lane; i < kABytes / 16; i += kNDec * 32) a4[i] = make_uint4(0, 0, 0, 0);
+          mbar_wait(b_aempty + 8 * b, (use - 1) & 1);
+          const uint32_t q0 = a_tile + tw * (kABytes / kTeamWarps);
+#pragma unroll
+          for (int r = 0; r < static_cast<int>(kABytes / kTeamWarps / 512); ++r) sts128_zero(q0 + 512 * r + 16 * lane);
         }
-        named_bar_sync(1, kNDec * 32);
-        const uint32_t t = static_cast<uint32_t>(un.rb) * p.tiles_k + kt;
-        const uint32_t a0 = __ldg(p.off + t), a1 = __ldg(p.off + t + 1);
-        uint32_t ng = 0;
-        if (e0 <= a0 && a0 <= a1 && a1 <= e1 && ((a1 - a0) & 31u) == 0) {
-          ng = (a1 - a0) >> 5;
-        } else if (dw == 0 && lane == 0) {
-          raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
+        if (tw == 0 && lane == 0) TRACE(1, gt);
+        named_bar_sync(1 + team, kTeamWarps * 32);
+        if (tw == 0 && lane == 0) {
+          TRACE(2, gt);
+          // every warp of the team is past its previous tile: hand its chunks back
+          for (uint32_t c = prev_base; c < prev_base + prev_n; ++c) mbar_arrive(eempty + 8 * (c % kRingT));
         }
-        for (uint32_t gi = dw; gi < ng; gi += kNDec) {
-          const uint32_t pos = a0 - e0 + gi * 32;
-          const uint32_t c = g_base + pos / kChunk;
-          while (nxt <= c) {
-            mbar_wait(bars.efull(nxt % p.ring), (nxt / p.ring) & 1);
+        if (a1 != a0 + 32 * ng && tw == 0 && lane == 0) raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
+        // contiguous quarter of the tile's groups
+        const uint32_t g0 = ng * tw / kTeamWarps, g1 = ng * (tw + 1) / kTeamWarps;
+        uint32_t g = g0;
+#ifdef TCSL_TRACE
+        long long wait_cyc = 0, n_waits = 0;
+#endif
+        for (; g + 4 <= g1; g += 4) {
+          const uint32_t c_hi = cbase + (32 * (g + 3)) / kChunk;
+#ifdef TCSL_TRACE
+          const long long tw0 = clock64();
+          if (nxt <= c_hi) ++n_waits;
+#endif
+          while (nxt <= c_hi) {
+            mbar_wait(efull + 8 * (nxt % kRingT), (nxt / kRingT) & 1);
             ++nxt;
           }
-          while (rel < c) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bars.eempty(rel % p.ring));
-            ++rel;
+#ifdef TCSL_TRACE
+          wait_cyc += clock64() - tw0;
+#endif
+          uint32_t e[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t pj = 32 * (g + j);
+            e[j] = lds32(ring + 4 * (((cbase + pj / kChunk) % kRingT) * kChunk + (pj % kChunk) + lane));
           }
-          const uint32_t e = ring_e[(c % p.ring) * kChunk + (pos % kChunk) + lane];
-          const uint32_t loc = e & 0xFFFFu;
-          if (loc < kMTB * kKTB) {
-            *reinterpret_cast<uint16_t*>(a_tile + a_offset(loc)) = static_cast<uint16_t>(e >> 16);
-          } else {
-            raise_dev(p.err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            err_or |= e[j];
+            sts16(a_tile + a_offset(e[j]), e[j] >> 16);
           }
         }
+        for (; g < g1; ++g) {
+          const uint32_t pj = 32 * g;
+          const uint32_t c = cbase + pj / kChunk;
+          while (nxt <= c) {
+            mbar_wait(efull + 8 * (nxt % kRingT), (nxt / kRingT) & 1);
+            ++nxt;
+          }
+          const uint32_t e = lds32(ring + 4 * ((c % kRingT) * kChunk + (pj % kChunk) + lane));
+          err_or |= e;
+          sts16(a_tile + a_offset(e), e >> 16);
+        }
+        if (tw == 0 && lane == 0) TRACE(3, gt);
+#ifdef TCSL_TRACE
+        if (tw == 0 && lane == 0 && blockIdx.x == 0 && p.trace && gt < 4096) {
+          p.trace[11 * 4096 + gt] = wait_cyc;
+          p.trace[12 * 4096 + gt] = n_waits;
+        }
+#endif
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bars.afull(b));
+        if (lane == 0) mbar_arrive(b_afull + 8 * b);
+        if (tw == 0 && lane == 0) TRACE(4, gt);
+        const uint32_t nch = (32 * ng + kChunk - 1) / kChunk;
+        prev_base = cbase;
+        prev_n = nch;
+        cbase += nch;
+        if (nxt < cbase) nxt = cbase;  // chunks of this tile that this warp never read
       }
-      // release every chunk of this unit (waiting for each first: see SURVEY-style
-      // phase rule — an arrival may only count toward the chunk it belongs to)
-      const uint32_t g_end = g_base + nchunks;
-      while (nxt < g_end) {
-        mbar_wait(bars.efull(nxt % p.ring), (nxt / p.ring) & 1);
-        ++nxt;
-      }
-      __syncwarp();
-      while (rel < g_end) {
-        if (lane == 0) mbar_arrive(bars.eempty(rel % p.ring));
-        ++rel;
-      }
-      g_base = g_end;
     }
+    // locations >= 8192 leave the 128x64 tile (the scatter masked them into range)
+    if (__any_sync(0xffffffffu, (err_or & 0xE000u) != 0) && lane == 0)
+      raise_dev(p.err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
   }
 
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, p.tmem_cols);
+    tmem_dealloc(tmem, C::kTmemCols);
   }
 }
 
@@ -369,7 +470,8 @@ int pad_n(int n) {
   if (n <= 16) return 16;
   if (n <= 32) return 32;
   if (n <= 64) return 64;
-  return std::min(256, (n + 63) / 64 * 64);
+  if (n <= 128) return 128;
+  return 256;
 }
 
 // Estimated runtime (us) of a split choice: max over persistent CTAs of their
@@ -390,7 +492,23 @@ double split_cost(int tiles_m, int tiles_k, int split, int sms, double t_tile, d
   return worst;
 }
 
+template <int NPAD>
+cudaError_t launch_npad(const Params& p, const CUtensorMap& tm, int grid, cudaStream_t s) {
+  using C = Cfg<NPAD>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(spmm_sm100_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::kSmem));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  spmm_sm100_kernel<NPAD><<<grid, kThreads, C::kSmem, s>>>(tm, p);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+unsigned long long* g_trace = nullptr;
 
 int num_sms() {
   static int sms = 0;
@@ -423,16 +541,11 @@ int auto_split(uint32_t m, uint32_t k, int n, double avg_entries_per_tile) {
 int spmm_sm100_plan(uint32_t m, uint32_t k, int n, int split_k, SpmmPlan* plan) {
   const int tiles_m = div_up_i(m, kMTB), tiles_k = div_up_i(k, kKTB);
   plan->n = n;
-  plan->n_pad = pad_n(n);
+  plan->n_pad = pad_n(std::min(n, 256));
   plan->split = split_k > 0 ? std::min(split_k, tiles_k) : 1;
   plan->units = tiles_m * plan->split;
   plan->grid = std::min(plan->units, num_sms());
-  const uint32_t x_stage = 64u * plan->n_pad * 2;
-  const int nx = std::max(2, std::min(8, static_cast<int>((48u * 1024) / x_stage)));
-  const size_t fixed = 1024 + static_cast<size_t>(kNA) * kABytes + static_cast<size_t>(nx) * x_stage;
-  int ring = static_cast<int>((200u * 1024 - fixed) / (kChunk * 4));
-  ring = std::max(4, std::min(32, ring));
-  plan->smem = fixed + static_cast<size_t>(ring) * kChunk * 4 + bar_bytes(nx, ring);
+  plan->smem = 0;
   return 0;
 }
 
@@ -455,59 +568,42 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
   p.out = out;
   p.ldo = plan.n;
   p.err = err;
-  const uint32_t x_stage_full = 64u * plan.n_pad * 2;
-  p.nx = std::max(2, std::min(8, static_cast<int>((48u * 1024) / x_stage_full)));
-  const size_t fixed = 1024 + static_cast<size_t>(kNA) * kABytes + static_cast<size_t>(p.nx) * x_stage_full;
-  p.ring = std::max(4, std::min(32, static_cast<int>((200u * 1024 - fixed) / (kChunk * 4))));
-
+  p.trace = g_trace;
   // Column slabs of <= 256 (one TMEM accumulator pair each).
   for (int col0 = 0; col0 < plan.n; col0 += 256) {
-    const int n_here = std::min(256, plan.n - col0);
-    const int n_pad = pad_n(n_here);
+    const int n_pad = pad_n(std::min(256, plan.n - col0));
+    const int box_w = std::min(n_pad, 64);
     p.col0 = col0;
-    p.n_pad = n_pad;
-    p.box_w = std::min(n_pad, 64);
-    p.x_boxes = n_pad / p.box_w;
-    p.x_box_bytes = 64u * p.box_w * 2;
-    p.x_stage = p.x_box_bytes * p.x_boxes;
-    uint32_t cols = 32;
-    while (cols < static_cast<uint32_t>(2 * n_pad)) cols <<= 1;
-    p.tmem_cols = cols;
-    p.idesc = idesc_f16_f32(128, n_pad, 1);
-    CUtensorMapSwizzle swz;
-    if (p.box_w == 8) {
-      swz = CU_TENSOR_MAP_SWIZZLE_NONE;
-      p.b_layout = 0;
-      p.b_lbo = 128;  // k-group (8 rows x 16 B) stride
-      p.b_sbo = 128;
-    } else {
-      const uint32_t row_bytes = p.box_w * 2;  // 32 / 64 / 128
-      swz = row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
-                            : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
-      p.b_layout = row_bytes == 32 ? 6u : (row_bytes == 64 ? 4u : 2u);
-      p.b_sbo = 8 * row_bytes;    // stride between 8-row k-groups
-      p.b_lbo = p.x_box_bytes;    // stride between 64-column atoms (n_pad > 64)
-    }
-    p.b_kstep = 16 * p.box_w * 2;  // 16 k-rows per MMA
+    const uint32_t row_bytes = box_w * 2;
+    const CUtensorMapSwizzle swz =
+        row_bytes == 16 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                        : (row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                           : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B));
     CUtensorMap tm;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(plan.n), static_cast<cuuint64_t>(k)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(p.box_w), 64u};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_w), 64u};
     cuuint32_t estr[2] = {1u, 1u};
     CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t*>(x), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    const size_t smem = 1024 + static_cast<size_t>(kNA) * kABytes + static_cast<size_t>(p.nx) * p.x_stage +
-                        static_cast<size_t>(p.ring) * kChunk * 4 + bar_bytes(p.nx, p.ring);
-    cudaError_t e = cudaFuncSetAttribute(spmm_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    spmm_sm100_kernel<<<plan.grid, kThreads, smem, s>>>(tm, p);
-    e = cudaGetLastError();
+    cudaError_t e;
+    switch (n_pad) {
+      case 8: e = launch_npad<8>(p, tm, plan.grid, s); break;
+      case 16: e = launch_npad<16>(p, tm, plan.grid, s); break;
+      case 32: e = launch_npad<32>(p, tm, plan.grid, s); break;
+      case 64: e = launch_npad<64>(p, tm, plan.grid, s); break;
+      case 128: e = launch_npad<128>(p, tm, plan.grid, s); break;
+      default: e = launch_npad<256>(p, tm, plan.grid, s); break;
+    }
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
 }  // namespace tcslk
+
+#ifdef TCSL_TRACE
+extern "C" void tcsl_cuda_debug_set_trace(unsigned long long* d_trace) { tcslk::g_trace = d_trace; }
+#endif
