@@ -8,16 +8,21 @@
 // reproduced (tolerance per BASELINE.json north_star), see spmm_exact for the
 // bit-exact CUDA-core mode.
 //
-// One persistent CTA per SM, warp-specialised (512 threads):
-//   warp 0      entry producer: streams each unit's contiguous entry span
-//               [off[t0], off[t1]) with cp.async.bulk into a ring of 2 KB chunks
-//   warp 1      X producer: TMA-loads the 64 x NPAD activation tile per k-tile
-//               (MN-major, hardware swizzle = 2*NPAD bytes)
-//   warp 2      TMEM owner + single-thread tcgen05.mma issuer (M=128, N=NPAD, K=16 x 4)
+// One persistent CTA per SM, warp-specialised (640 threads):
+//   warp 0      X producer: TMA-loads 256 k-rows x NPAD of the activations per
+//               stage (MN-major, hardware swizzle = 2*NPAD bytes)
+//   warp 1      TMEM owner + single-thread tcgen05.mma issuer (M=128, N=NPAD, K=16 x 4
+//               per k-tile). Its loop is the pacing resource (a tcgen05.mma of this
+//               shape occupies the tensor pipe ~45 cycles), so it polls cheap smem
+//               flags instead of mbarriers and commits once per k-tile.
+//   warp 2      L2 prefetcher: cp.async.bulk.prefetch.L2 of the entry spans of the
+//               next kPrefetchAhead k-tiles, paced by the MMA's progress
 //   warps 4-7   epilogue: tcgen05.ld accumulator -> fp32 Y rows (or split-K partials)
-//   warps 8-15  decode, two teams of 4 warps working on alternate k-tiles: zero
-//               the dense tile, then scatter each 32-entry group (one entry per
-//               lane) into the SWIZZLE_NONE K-major core-matrix layout
+//   warps 8-19  decode, three teams of 4 warps on k-tiles gt % 3 == team: zero the
+//               dense tile, then each warp scatters its contiguous quarter of the
+//               tile's 32-entry groups (one entry per lane, loaded straight from
+//               L2 into registers one team-tile ahead) into the SWIZZLE_NONE
+//               K-major core-matrix layout.
 // The core-matrix layout puts element (x, y) in bank (x%8)*4 + (y%8)/2, which is
 // exactly the reference's bank_id (proj/include/tcsl/tcsl_format.hpp:18), so the
 // encoder's ahead-of-time bank reordering keeps the scatter near one wavefront
@@ -30,6 +35,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "sm100_ptx.cuh"
@@ -41,35 +47,44 @@ namespace {
 
 constexpr int kMTB = 128, kKTB = 64;
 constexpr uint32_t kABytes = kMTB * kKTB * 2;  // dense fp16 tile, 16 KB
-constexpr int kNA = 4;                         // dense-tile buffers (2 per decode team)
-constexpr int kTeamWarps = 4;                  // warps per decode team
-constexpr uint32_t kChunk = 512;               // entries per ring chunk (2 KB); chunks are tile-aligned
-constexpr uint32_t kRingT = 20;                // chunks per team ring (40 KB; >= one dense tile + slack)
-constexpr int kThreads = 512;
-constexpr int kWarpEpi = 4, kWarpDec = 8;
+constexpr int kTeams = 3;                      // decode teams
+constexpr int kTeamWarps = 4;                  // warps per team
+// Warp roles. The scheduler favours higher warp ids, so the MMA issuer — the
+// pacing resource — gets the highest id; decode warps take the low ids.
+constexpr int kWarpDec = 0;                                 // 12 decode warps: 0..11
+constexpr int kWarpEpi = kTeams * kTeamWarps;               // 4 epilogue warps: 12..15 (id % 4 = TMEM quarter)
+constexpr int kWarpX = kWarpEpi + 4;                        // 16: X producer
+constexpr int kWarpPf = kWarpX + 1;                         // 17: L2 prefetcher
+constexpr int kWarpMma = kWarpX + 3;                        // 19: TMEM owner + MMA issuer
+constexpr int kThreads = 32 * (kWarpMma + 1);
+constexpr int kChunkG = 16;                    // groups per warp per register chunk
+constexpr int kPrefetchAhead = 24;             // k-tiles of entries kept in flight toward L2
 
 template <int NPAD>
 struct Cfg {
   static constexpr int kBoxW = NPAD < 64 ? NPAD : 64;       // TMA box / swizzle atom width
   static constexpr int kBoxes = NPAD / kBoxW;
-  static constexpr uint32_t kBoxBytes = 64u * kBoxW * 2;    // 64 k-rows
+  static constexpr int kTX = NPAD <= 64 ? 4 : 1;             // k-tiles per X stage
+  static constexpr uint32_t kBoxBytes = 64u * kTX * kBoxW * 2;
   static constexpr uint32_t kXStage = kBoxBytes * kBoxes;
-  static constexpr int kNX = (32768 / kXStage) < 2 ? 2 : ((32768 / kXStage) > 8 ? 8 : (32768 / kXStage));
+  static constexpr int kNX = (65536 / kXStage) < 2 ? 2 : ((65536 / kXStage) > 4 ? 4 : (65536 / kXStage));
+  static constexpr int kNA = kTeams * (NPAD <= 64 ? 3 : 2);  // dense-tile buffers
   static constexpr uint32_t kRowBytes = kBoxW * 2;
   static constexpr uint32_t kLayout = kRowBytes == 16 ? 0u : (kRowBytes == 32 ? 6u : (kRowBytes == 64 ? 4u : 2u));
   // SWIZZLE_NONE (NPAD=8): LBO = k-group stride (8 rows x 16 B); swizzled: SBO = 8-row
   // k-group stride, LBO = stride between 64-column atoms.
   static constexpr uint32_t kLBO = kRowBytes == 16 ? 128u : kBoxBytes;
   static constexpr uint32_t kSBO = kRowBytes == 16 ? 128u : 8u * kRowBytes;
-  static constexpr uint32_t kKStep = 16u * kRowBytes;       // 16 k-rows per MMA
+  static constexpr uint32_t kKStep = 16u * kRowBytes;        // 16 k-rows per MMA
+  static constexpr uint32_t kTileStep = 64u * kRowBytes;     // next k-tile inside a stage
   static constexpr uint32_t kTmemCols = (2 * NPAD) <= 32 ? 32 : ((2 * NPAD) <= 64 ? 64 : ((2 * NPAD) <= 128 ? 128 : ((2 * NPAD) <= 256 ? 256 : 512)));
   static constexpr uint32_t kIdesc = idesc_f16_f32(128, NPAD, 1);
   // smem carve-up (from a 1024-aligned base)
   static constexpr uint32_t kOffX = kNA * kABytes;
-  static constexpr uint32_t kOffE = kOffX + kNX * kXStage;
-  static constexpr uint32_t kOffBar = kOffE + 2 * kRingT * kChunk * 4;
-  static constexpr uint32_t kNumBars = 2 * kNA + 2 * kNX + 4 * kRingT + 4;
-  static constexpr uint32_t kSmem = 1024 + kOffBar + 8 * kNumBars + 16;
+  static constexpr uint32_t kOffBar = kOffX + kNX * kXStage;
+  static constexpr uint32_t kNumBars = kNA + 2 * kNX + 4;
+  static constexpr uint32_t kOffFlags = kOffBar + 8 * kNumBars;
+  static constexpr uint32_t kSmem = 1024 + kOffFlags + 4 * kNA + 16;
 };
 
 struct Params {
@@ -83,7 +98,14 @@ struct Params {
   int ldo;
   int* err;
   unsigned long long* trace;  // TCSL_TRACE builds only: per-event clock64 stamps of CTA 0
+  int debug;                  // TCSL_TRACE builds only: 1 MMA ignores decode, 2 no scatter, 4 no zeroing
 };
+
+#ifdef TCSL_TRACE
+#define DBG(bit) (p.debug & (bit))
+#else
+#define DBG(bit) 0
+#endif
 
 #ifdef TCSL_TRACE
 #define TRACE(slot, idx) \
@@ -103,22 +125,43 @@ __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
   x.kt1 = static_cast<int>(static_cast<long long>(x.s + 1) * p.tiles_k / p.split);
   return x;
 }
-// The unit's entry span; every role derives the same (sanitised) span.
-__device__ __forceinline__ bool unit_span(const Params& p, const Unit& u, uint32_t& e0, uint32_t& e1) {
-  const uint32_t t0 = static_cast<uint32_t>(u.rb) * p.tiles_k + u.kt0;
-  const uint32_t t1 = static_cast<uint32_t>(u.rb) * p.tiles_k + u.kt1;
-  e0 = __ldg(p.off + t0);
-  e1 = __ldg(p.off + t1);
-  if (e1 < e0 || e1 > p.n_entries || (e0 & 31u) || ((e1 - e0) & 31u)) {
-    e1 = e0;
-    return false;
+
+// Walks this CTA's k-tiles in schedule order: (unit, kt, global tile index t).
+struct TileWalk {
+  int u, kt, kt1;
+  uint32_t t;
+  __device__ __forceinline__ bool start(const Params& p) {
+    u = blockIdx.x;
+    return load(p);
   }
-  return true;
-}
-// A tile's span is streamed / decoded only when it sits inside the unit span
-// as whole 32-entry groups; producer and decoders apply the same rule.
-__device__ __forceinline__ uint32_t tile_groups(uint32_t e0, uint32_t e1, uint32_t a0, uint32_t a1) {
-  return (e0 <= a0 && a0 <= a1 && a1 <= e1 && ((a1 - a0) & 31u) == 0) ? (a1 - a0) >> 5 : 0u;
+  __device__ __forceinline__ bool load(const Params& p) {
+    if (u >= p.units) return false;
+    const Unit un = unit_of(p, u);
+    kt = un.kt0;
+    kt1 = un.kt1;
+    t = static_cast<uint32_t>(un.rb) * p.tiles_k + un.kt0;
+    return true;
+  }
+  // advance by `steps` tiles (crossing units as needed)
+  __device__ __forceinline__ bool advance(const Params& p, int steps) {
+    while (steps > 0) {
+      const int left = kt1 - kt;
+      if (steps < left) {
+        kt += steps;
+        t += steps;
+        return true;
+      }
+      steps -= left;
+      u += gridDim.x;
+      if (!load(p)) return false;
+    }
+    return true;
+  }
+};
+
+// Number of 32-entry groups of tile [a0, a1); 0 when malformed.
+__device__ __forceinline__ uint32_t tile_groups(const Params& p, uint32_t a0, uint32_t a1) {
+  return (a0 <= a1 && a1 <= p.n_entries && ((a1 - a0) & 31u) == 0) ? (a1 - a0) >> 5 : 0u;
 }
 
 // Byte offset of tile element `loc` (= x*64 + y) in the K-major SWIZZLE_NONE
@@ -130,98 +173,84 @@ __device__ __forceinline__ uint32_t a_offset(uint32_t loc) {
          | ((loc << 4) & 0x380u);  // (y/8)*128 from loc[5:3]
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_smem(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_smem_add(uint32_t addr, uint32_t v) {
+  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_shared_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+// Spin on an smem counter until it reaches `target` (watchdog as in mbar_wait).
+__device__ __forceinline__ void wait_counter(uint32_t addr, uint32_t target) {
+  if (static_cast<int32_t>(ld_acquire_smem(addr) - target) >= 0) return;
+  const long long t0 = clock64();
+  while (static_cast<int32_t>(ld_acquire_smem(addr) - target) < 0) {
+    if (clock64() - t0 > 40000000000LL) __trap();
+  }
+}
+
 template <int NPAD>
 __global__ void __launch_bounds__(kThreads, 1)
     spmm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
   using C = Cfg<NPAD>;
+  constexpr int NA = C::kNA;
+  constexpr int NX = C::kNX;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t s_a = (raw + 1023u) & ~1023u;
   const uint32_t s_x = s_a + C::kOffX;
-  const uint32_t s_e = s_a + C::kOffE;  // team t ring at s_e + t * kRingT * kChunk * 4
   const uint32_t s_bar = s_a + C::kOffBar;
-  const uint32_t b_afull = s_bar, b_aempty = s_bar + 8 * kNA;
-  const uint32_t b_xfull = s_bar + 8 * (2 * kNA), b_xempty = b_xfull + 8 * C::kNX;
-  const uint32_t b_efull = b_xempty + 8 * C::kNX;  // [team][kRingT]
-  const uint32_t b_eempty = b_efull + 8 * 2 * kRingT;
-  const uint32_t b_dfull = b_eempty + 8 * 2 * kRingT, b_dempty = b_dfull + 16;
-  const uint32_t s_tmem_slot = b_dempty + 16;
+  const uint32_t b_aempty = s_bar;  // [NA]   MMA of the buffer's last tile complete
+  const uint32_t b_xfull = s_bar + 8 * NA, b_xempty = b_xfull + 8 * NX;
+  const uint32_t b_dfull = b_xempty + 8 * NX, b_dempty = b_dfull + 16;
+  const uint32_t s_flags = s_a + C::kOffFlags;  // [NA] decode-warp completions per buffer
+  const uint32_t s_tmem_slot = s_flags + 4 * NA;
+  const uint32_t s_progress = s_tmem_slot + 4;  // k-tiles the MMA has consumed (prefetch pacing)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (s_tmem_slot - raw));
+  volatile uint32_t* progress = reinterpret_cast<volatile uint32_t*>(smem_raw + (s_progress - raw));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kNA; ++i) {
-      mbar_init(b_afull + 8 * i, kTeamWarps);
+    for (int i = 0; i < NA; ++i) {
       mbar_init(b_aempty + 8 * i, 1);
+      st_shared_u32(s_flags + 4 * i, 0);
     }
-    for (int i = 0; i < C::kNX; ++i) {
+    for (int i = 0; i < NX; ++i) {
       mbar_init(b_xfull + 8 * i, 1);
       mbar_init(b_xempty + 8 * i, 1);
-    }
-    for (uint32_t i = 0; i < 2 * kRingT; ++i) {
-      mbar_init(b_efull + 8 * i, 1);
-      mbar_init(b_eempty + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(b_dfull + 8 * i, 1);
       mbar_init(b_dempty + 8 * i, 4);
     }
+    *progress = 0;
     fence_barrier_init();
   }
-  if (warp == 1 && lane == 0) prefetch_tmap(&tmap_x);
-  if (warp == 2) tmem_alloc_dyn(s_tmem_slot, C::kTmemCols);
-  for (uint32_t i = threadIdx.x; i < kNA * kABytes / 16; i += kThreads) sts128_zero(s_a + 16 * i);
+  if (warp == kWarpX && lane == 0) prefetch_tmap(&tmap_x);
+  if (warp == kWarpMma) tmem_alloc_dyn(s_tmem_slot, C::kTmemCols);
+  for (uint32_t i = threadIdx.x; i < NA * kABytes / 16; i += kThreads) sts128_zero(s_a + 16 * i);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 || warp == 3) {
-    // ------------------------------------------------------ entry producers (one per team)
-    // Streams the entry span of every k-tile of its team (gt % 2 == team) into
-    // the team ring, in tile-aligned 2 KB chunks.
-    if (lane == 0) {
-      const uint32_t team = warp == 0 ? 0u : 1u;
-      const uint32_t ring = s_e + team * kRingT * kChunk * 4;
-      const uint32_t efull = b_efull + 8 * team * kRingT, eempty = b_eempty + 8 * team * kRingT;
-      const uint64_t pol = policy_evict_first();
-      uint32_t g = 0, gt = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const Unit un = unit_of(p, u);
-        uint32_t e0, e1;
-        if (!unit_span(p, un, e0, e1) && team == 0) raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
-        const uint32_t tile0 = static_cast<uint32_t>(un.rb) * p.tiles_k + un.kt0;
-        for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
-          if ((gt & 1u) != team) continue;
-          const uint32_t t = tile0 + (kt - un.kt0);
-          const uint32_t a0 = __ldg(p.off + t), a1 = __ldg(p.off + t + 1);
-          const uint32_t ng = tile_groups(e0, e1, a0, a1);
-          for (uint32_t c0 = 0; c0 < 32 * ng; c0 += kChunk, ++g) {
-            const uint32_t slot = g % kRingT;
-            const uint32_t use = g / kRingT;
-            if (team == 0) TRACE(9, g);
-            if (use > 0) mbar_wait_sleep(eempty + 8 * slot, (use - 1) & 1);
-            if (team == 0) TRACE(10, g);
-            const uint32_t bytes = min(kChunk, 32 * ng - c0) * 4;
-            mbar_arrive_expect_tx(efull + 8 * slot, bytes);
-            bulk_g2s(ring + slot * kChunk * 4, p.ent + a0 + c0, bytes, efull + 8 * slot, pol);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
+  if (warp == kWarpX) {
     // ---------------------------------------------------------------- X producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_last();
-      uint32_t gt = 0;
+      uint32_t gs = 0;  // global X stage counter
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const Unit un = unit_of(p, u);
-        for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
-          const uint32_t slot = gt % C::kNX;
-          const uint32_t use = gt / C::kNX;
+        for (int kt = un.kt0; kt < un.kt1; kt += C::kTX, ++gs) {
+          const uint32_t slot = gs % NX;
+          const uint32_t use = gs / NX;
           if (use > 0) mbar_wait_sleep(b_xempty + 8 * slot, (use - 1) & 1);
           mbar_arrive_expect_tx(b_xfull + 8 * slot, C::kXStage);
 #pragma unroll
@@ -231,46 +260,63 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 2) {
+  } else if (warp == kWarpMma) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      uint32_t gt = 0, ui = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
-        const Unit un = unit_of(p, u);
-        const uint32_t acc = ui & 1;
-        if (ui >= 2) mbar_wait_sleep(b_dempty + 8 * acc, ((ui >> 1) - 1) & 1);
+    // The whole warp walks the schedule (warp-uniform values stay in uniform
+    // registers); one elected lane issues. Descriptors are base + byte offset/16.
+    const uint64_t a_desc0 = smem_desc(s_a, 128, 1024, 0);
+    const uint64_t b_desc0 = smem_desc(s_x, C::kLBO, C::kSBO, C::kLayout);
+    uint32_t gt = 0, ui = 0, gs = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
+      const Unit un = unit_of(p, u);
+      const uint32_t acc = ui & 1;
+      if (ui >= 2) mbar_wait_sleep(b_dempty + 8 * acc, ((ui >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * NPAD;
+      for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
+        const int in_stage = (kt - un.kt0) % C::kTX;
+        const uint32_t xs = gs % NX;
+        if (in_stage == 0) mbar_wait(b_xfull + 8 * xs, (gs / NX) & 1);
+        const uint32_t b = gt % NA;
+        if (lane == 0) TRACE(5, gt);
+        if (!DBG(1)) wait_counter(s_flags + 4 * b, kTeamWarps * (gt / NA + 1));
+        if (lane == 0) TRACE(6, gt);
         tc_fence_after();
-        const uint32_t d_tmem = tmem + acc * NPAD;
-        for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
-          const uint32_t b = gt % kNA;
-          const uint32_t xs = gt % C::kNX;
-          TRACE(5, gt);
-          mbar_wait(b_afull + 8 * b, (gt / kNA) & 1);
-          TRACE(6, gt);
-          mbar_wait(b_xfull + 8 * xs, (gt / C::kNX) & 1);
-          TRACE(7, gt);
-          tc_fence_after();
-          const uint32_t a0 = s_a + b * kABytes;
-          const uint32_t x0 = s_x + xs * C::kXStage;
+        const uint64_t ad = a_desc0 + ((b * kABytes) >> 4);
+        const uint64_t bd = b_desc0 + ((xs * C::kXStage + in_stage * C::kTileStep) >> 4);
+        if (elect_one()) {
 #pragma unroll
-          for (int s = 0; s < kKTB / 16; ++s) {
-            const uint64_t ad = smem_desc(a0 + s * 256, 128, 1024, 0);
-            const uint64_t bd = smem_desc(x0 + s * C::kKStep, C::kLBO, C::kSBO, C::kLayout);
-            mma_f16_ss(d_tmem, ad, bd, C::kIdesc, (kt > un.kt0 || s > 0) ? 1u : 0u);
-          }
+          for (int s = 0; s < kKTB / 16; ++s)
+            mma_f16_ss(d_tmem, ad + (s * 256 >> 4), bd + (s * C::kKStep >> 4), C::kIdesc,
+                       (kt > un.kt0 || s > 0) ? 1u : 0u);
           mma_commit(b_aempty + 8 * b);
-          mma_commit(b_xempty + 8 * xs);
-#ifdef TCSL_TRACE
-          if (blockIdx.x == 0 && p.trace) {  // debug only: measure MMA completion latency
-            mbar_wait(b_aempty + 8 * b, (gt / kNA) & 1);
-            TRACE(8, gt);
-          }
-#endif
+          if (in_stage == C::kTX - 1 || kt + 1 == un.kt1) mma_commit(b_xempty + 8 * xs);
+          *progress = gt + 1;
         }
-        mma_commit(b_dfull + 8 * acc);
+        __syncwarp();
+        if (in_stage == C::kTX - 1 || kt + 1 == un.kt1) ++gs;
+        if (lane == 0) TRACE(7, gt);
+      }
+      if (elect_one()) mma_commit(b_dfull + 8 * acc);
+      __syncwarp();
+    }
+  } else if (warp == kWarpPf) {
+    // ---------------------------------------------------------------- L2 prefetcher
+    // Keeps the entry spans of the next kPrefetchAhead k-tiles on their way to
+    // L2 so the decode warps' loads hit L2 instead of waiting on HBM.
+    if (lane == 0) {
+      TileWalk w;
+      uint32_t issued = 0;
+      bool more = w.start(p);
+      while (more) {
+        while (issued >= *progress + kPrefetchAhead) __nanosleep(256);
+        const uint32_t a0 = __ldg(p.off + w.t), a1 = __ldg(p.off + w.t + 1);
+        const uint32_t ng = tile_groups(p, a0, a1);
+        if (ng) bulk_prefetch_l2(p.ent + a0, ng * 128u);
+        ++issued;
+        more = w.advance(p, 1);
       }
     }
-    __syncwarp();
   } else if (warp >= kWarpEpi && warp < kWarpEpi + 4) {
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lanes 32q..32q+31
@@ -326,128 +372,107 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(b_dempty + 8 * acc);
     }
-  } else if (warp >= kWarpDec) {
-    // ---------------------------------------------------------------- decode
-    // Team t (4 warps) decodes the k-tiles with gt % 2 == t into buffers t, t+2.
+  } else if (warp >= kWarpDec && warp < kWarpDec + kTeams * kTeamWarps) {
+    // ---------------------------------------------------------------- decode teams
+    // Team t owns the k-tiles gt = t, t + kTeams, ...; each of its 4 warps owns a
+    // contiguous quarter of the tile's groups. Entry loads run one register chunk
+    // ahead across team-tiles and offsets two team-tiles ahead, so L2 latency
+    // stays off the critical path.
     const int dw = warp - kWarpDec;
-    const uint32_t team = dw / kTeamWarps;
+    const int team = dw / kTeamWarps;
     const int tw = dw % kTeamWarps;
-    const uint32_t ring = s_e + team * kRingT * kChunk * 4;
-    const uint32_t efull = b_efull + 8 * team * kRingT, eempty = b_eempty + 8 * team * kRingT;
-    uint32_t gt = 0;
-    uint32_t cbase = 0;                   // first team-ring chunk of the current tile
-    uint32_t prev_base = 0, prev_n = 0;   // chunks of this team's previous tile (released after the barrier)
-    uint32_t nxt = 0;                     // team-ring chunks < nxt have been waited full by this warp
+    TileWalk w;
+    bool more = w.start(p) && w.advance(p, team);
+    uint32_t gt = team;
     uint32_t err_or = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const Unit un = unit_of(p, u);
-      uint32_t e0, e1;
-      unit_span(p, un, e0, e1);
-      const uint32_t tile0 = static_cast<uint32_t>(un.rb) * p.tiles_k + un.kt0;
-      const int ntiles = un.kt1 - un.kt0;
-      // offsets window: lane l holds off[tile0 + 32*w + l]
-      const uint32_t last_off = tile0 + ntiles;
-      uint32_t win_cur = __ldg(p.off + min(tile0 + lane, last_off));
-      uint32_t win_nxt = __ldg(p.off + min(tile0 + 32 + lane, last_off));
-      int win = 0;
-      for (int i = 0; i < ntiles; ++i, ++gt) {
-        if ((i >> 5) != win) {  // slide the window by 32 tiles
-          win_cur = win_nxt;
-          ++win;
-          win_nxt = __ldg(p.off + min(tile0 + 32 * (win + 1) + lane, last_off));
-        }
-        if ((gt & 1u) != team) continue;
-        const uint32_t a0 = __shfl_sync(0xffffffffu, win_cur, i & 31);
-        const uint32_t a1n = __shfl_sync(0xffffffffu, win_nxt, 0);
-        const uint32_t a1c = __shfl_sync(0xffffffffu, win_cur, (i + 1) & 31);
-        const uint32_t a1 = ((i & 31) == 31) ? a1n : a1c;
-        const uint32_t ng = tile_groups(e0, e1, a0, a1);
-        const uint32_t b = gt % kNA;
-        const uint32_t use = gt / kNA;
-        const uint32_t a_tile = s_a + b * kABytes;
-        if (tw == 0 && lane == 0) TRACE(0, gt);
-        if (use > 0) {
-          mbar_wait(b_aempty + 8 * b, (use - 1) & 1);
-          const uint32_t q0 = a_tile + tw * (kABytes / kTeamWarps);
+    bool bad_off = false;
+    uint32_t a0 = 0, a1 = 0, n0 = 0, n1 = 0;
+    uint32_t e[kChunkG];
+    bool has_n = false;
+    if (more) {
+      a0 = __ldg(p.off + w.t);
+      a1 = __ldg(p.off + w.t + 1);
+      const uint32_t ng = tile_groups(p, a0, a1);
+      const uint32_t g0 = ng * tw / kTeamWarps, g1 = ng * (tw + 1) / kTeamWarps;
 #pragma unroll
-          for (int r = 0; r < static_cast<int>(kABytes / kTeamWarps / 512); ++r) sts128_zero(q0 + 512 * r + 16 * lane);
-        }
-        if (tw == 0 && lane == 0) TRACE(1, gt);
-        named_bar_sync(1 + team, kTeamWarps * 32);
-        if (tw == 0 && lane == 0) {
-          TRACE(2, gt);
-          // every warp of the team is past its previous tile: hand its chunks back
-          for (uint32_t c = prev_base; c < prev_base + prev_n; ++c) mbar_arrive(eempty + 8 * (c % kRingT));
-        }
-        if (a1 != a0 + 32 * ng && tw == 0 && lane == 0) raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
-        // contiguous quarter of the tile's groups
-        const uint32_t g0 = ng * tw / kTeamWarps, g1 = ng * (tw + 1) / kTeamWarps;
-        uint32_t g = g0;
-#ifdef TCSL_TRACE
-        long long wait_cyc = 0, n_waits = 0;
-#endif
-        for (; g + 4 <= g1; g += 4) {
-          const uint32_t c_hi = cbase + (32 * (g + 3)) / kChunk;
-#ifdef TCSL_TRACE
-          const long long tw0 = clock64();
-          if (nxt <= c_hi) ++n_waits;
-#endif
-          while (nxt <= c_hi) {
-            mbar_wait(efull + 8 * (nxt % kRingT), (nxt / kRingT) & 1);
-            ++nxt;
-          }
-#ifdef TCSL_TRACE
-          wait_cyc += clock64() - tw0;
-#endif
-          uint32_t e[4];
+      for (int j = 0; j < kChunkG; ++j)
+        e[j] = (g0 + j < g1) ? ldg_stream(p.ent + a0 + 32 * (g0 + j) + lane) : 0u;
+      has_n = w.advance(p, kTeams);
+      if (has_n) {
+        n0 = __ldg(p.off + w.t);
+        n1 = __ldg(p.off + w.t + 1);
+      }
+    }
+    while (more) {
+      const uint32_t ng = tile_groups(p, a0, a1);
+      if (a1 != a0 + 32 * ng) bad_off = true;
+      const uint32_t g0 = ng * tw / kTeamWarps, g1 = ng * (tw + 1) / kTeamWarps;
+      // offsets of the team's tile after next
+      const bool has_nn = has_n && w.advance(p, kTeams);
+      uint32_t nn0 = 0, nn1 = 0;
+      if (has_nn) {
+        nn0 = __ldg(p.off + w.t);
+        nn1 = __ldg(p.off + w.t + 1);
+      }
+      const uint32_t nng = has_n ? tile_groups(p, n0, n1) : 0u;
+      const uint32_t ng0 = nng * tw / kTeamWarps, ng1 = nng * (tw + 1) / kTeamWarps;
+
+      const uint32_t b = gt % NA;
+      const uint32_t use = gt / NA;
+      const uint32_t a_tile = s_a + b * kABytes;
+      if (tw == 0 && lane == 0) TRACE(0, gt);
+      if (use > 0 && !DBG(4)) {
+        mbar_wait(b_aempty + 8 * b, (use - 1) & 1);
+        const uint32_t q0 = a_tile + tw * (kABytes / kTeamWarps);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t pj = 32 * (g + j);
-            e[j] = lds32(ring + 4 * (((cbase + pj / kChunk) % kRingT) * kChunk + (pj % kChunk) + lane));
-          }
+        for (int r = 0; r < static_cast<int>(kABytes / kTeamWarps / 512); ++r) sts128_zero(q0 + 512 * r + 16 * lane);
+      }
+      if (tw == 0 && lane == 0) TRACE(1, gt);
+      named_bar_sync(1 + team, kTeamWarps * 32);
+      if (tw == 0 && lane == 0) TRACE(2, gt);
+      uint32_t c0 = g0;
+      do {
+        // the chunk after this one: rest of my quarter, else my quarter of the next team-tile
+        uint32_t f[kChunkG];
+        const bool same = c0 + kChunkG < g1;
+        const uint32_t* fsrc = same ? p.ent + a0 + 32 * (c0 + kChunkG) + lane : p.ent + n0 + 32 * ng0 + lane;
+        const uint32_t fcnt = same ? g1 - c0 - kChunkG : ng1 - ng0;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kChunkG; ++j) f[j] = (static_cast<uint32_t>(j) < fcnt) ? ldg_stream(fsrc + 32 * j) : 0u;
+        const uint32_t cnt = g1 - c0;  // may exceed kChunkG; only the first kChunkG are in e[]
+#pragma unroll
+        for (int j = 0; j < kChunkG; ++j) {
+          if (static_cast<uint32_t>(j) < cnt && !DBG(2)) {
             err_or |= e[j];
             sts16(a_tile + a_offset(e[j]), e[j] >> 16);
           }
         }
-        for (; g < g1; ++g) {
-          const uint32_t pj = 32 * g;
-          const uint32_t c = cbase + pj / kChunk;
-          while (nxt <= c) {
-            mbar_wait(efull + 8 * (nxt % kRingT), (nxt / kRingT) & 1);
-            ++nxt;
-          }
-          const uint32_t e = lds32(ring + 4 * ((c % kRingT) * kChunk + (pj % kChunk) + lane));
-          err_or |= e;
-          sts16(a_tile + a_offset(e), e >> 16);
-        }
-        if (tw == 0 && lane == 0) TRACE(3, gt);
-#ifdef TCSL_TRACE
-        if (tw == 0 && lane == 0 && blockIdx.x == 0 && p.trace && gt < 4096) {
-          p.trace[11 * 4096 + gt] = wait_cyc;
-          p.trace[12 * 4096 + gt] = n_waits;
-        }
-#endif
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(b_afull + 8 * b);
-        if (tw == 0 && lane == 0) TRACE(4, gt);
-        const uint32_t nch = (32 * ng + kChunk - 1) / kChunk;
-        prev_base = cbase;
-        prev_n = nch;
-        cbase += nch;
-        if (nxt < cbase) nxt = cbase;  // chunks of this tile that this warp never read
-      }
+#pragma unroll
+        for (int j = 0; j < kChunkG; ++j) e[j] = f[j];
+        c0 += kChunkG;
+      } while (c0 < g1);
+      if (tw == 0 && lane == 0) TRACE(3, gt);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) red_release_smem_add(s_flags + 4 * b, 1u);
+      if (tw == 0 && lane == 0) TRACE(4, gt);
+      more = has_n;
+      a0 = n0;
+      a1 = n1;
+      has_n = has_nn;
+      n0 = nn0;
+      n1 = nn1;
+      gt += kTeams;
     }
     // locations >= 8192 leave the 128x64 tile (the scatter masked them into range)
     if (__any_sync(0xffffffffu, (err_or & 0xE000u) != 0) && lane == 0)
       raise_dev(p.err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
+    if (__any_sync(0xffffffffu, bad_off) && lane == 0) raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == kWarpMma) {
     tc_fence_after();
     tmem_dealloc(tmem, C::kTmemCols);
   }
@@ -495,6 +520,7 @@ double split_cost(int tiles_m, int tiles_k, int split, int sms, double t_tile, d
 template <int NPAD>
 cudaError_t launch_npad(const Params& p, const CUtensorMap& tm, int grid, cudaStream_t s) {
   using C = Cfg<NPAD>;
+  static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(spmm_sm100_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -523,8 +549,8 @@ int num_sms() {
 int auto_split(uint32_t m, uint32_t k, int n, double avg_entries_per_tile) {
   const int tiles_m = div_up_i(m, kMTB), tiles_k = div_up_i(k, kKTB);
   const int sms = num_sms();
-  // per-SM streaming rate ~ 6.5 TB/s / 148; dense-tile smem floor ~0.12 us per tile
-  const double t_tile = std::max(avg_entries_per_tile * 4.0 / 44.0e3, 0.12);
+  // per-SM streaming rate ~ 6.5 TB/s / 148; MMA floor ~0.1 us per tile
+  const double t_tile = std::max(avg_entries_per_tile * 4.0 / 44.0e3, 0.1);
   const double mn_bytes = static_cast<double>(m) * std::min(n, 256) * 4.0;
   int best = 1;
   double best_cost = split_cost(tiles_m, tiles_k, 1, sms, t_tile, mn_bytes);
@@ -569,10 +595,14 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
   p.ldo = plan.n;
   p.err = err;
   p.trace = g_trace;
+#ifdef TCSL_TRACE
+  p.debug = getenv("TCSL_DEBUG") ? atoi(getenv("TCSL_DEBUG")) : 0;
+#endif
   // Column slabs of <= 256 (one TMEM accumulator pair each).
   for (int col0 = 0; col0 < plan.n; col0 += 256) {
     const int n_pad = pad_n(std::min(256, plan.n - col0));
     const int box_w = std::min(n_pad, 64);
+    const int box_rows = n_pad <= 64 ? 256 : 64;  // Cfg<NPAD>::kTX k-tiles per stage
     p.col0 = col0;
     const uint32_t row_bytes = box_w * 2;
     const CUtensorMapSwizzle swz =
@@ -582,7 +612,7 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
     CUtensorMap tm;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(plan.n), static_cast<cuuint64_t>(k)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_w), 64u};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_rows)};
     cuuint32_t estr[2] = {1u, 1u};
     CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t*>(x), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
