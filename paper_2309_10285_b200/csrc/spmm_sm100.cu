@@ -8,24 +8,27 @@
 // reproduced (tolerance per BASELINE.json north_star), see spmm_exact for the
 // bit-exact CUDA-core mode.
 //
-// One persistent CTA per SM, warp-specialised (640 threads):
-//   warp 0      X producer: TMA-loads 256 k-rows x NPAD of the activations per
-//               stage (MN-major, hardware swizzle = 2*NPAD bytes)
-//   warp 1      TMEM owner + single-thread tcgen05.mma issuer (M=128, N=NPAD, K=16 x 4
-//               per k-tile). Its loop is the pacing resource (a tcgen05.mma of this
-//               shape occupies the tensor pipe ~45 cycles), so it polls cheap smem
-//               flags instead of mbarriers and commits once per k-tile.
-//   warp 2      L2 prefetcher: cp.async.bulk.prefetch.L2 of the entry spans of the
+// One persistent CTA per SM, warp-specialised (640 threads). The scheduler
+// favours higher warp ids, so the pacing role gets the highest id:
+//   warps 0-11  decode, three teams of 4 warps on k-tiles gt % 3 == team: zero the
+//               dense tile, then each warp scatters its contiguous share of the
+//               tile's 32-entry groups (one entry per lane, loaded from L2 straight
+//               into registers one team-tile ahead) into the SWIZZLE_NONE K-major
+//               core-matrix layout
+//   warps 12-15 epilogue: tcgen05.ld accumulator -> fp32 Y rows (or split-K partials)
+//   warp 16     X producer: TMA-loads kTX k-tiles x NPAD activations per stage
+//               (MN-major, hardware swizzle = 2*NPAD bytes)
+//   warp 17     L2 prefetcher: cp.async.bulk.prefetch.L2 of the entry spans of the
 //               next kPrefetchAhead k-tiles, paced by the MMA's progress
-//   warps 4-7   epilogue: tcgen05.ld accumulator -> fp32 Y rows (or split-K partials)
-//   warps 8-19  decode, three teams of 4 warps on k-tiles gt % 3 == team: zero the
-//               dense tile, then each warp scatters its contiguous quarter of the
-//               tile's 32-entry groups (one entry per lane, loaded straight from
-//               L2 into registers one team-tile ahead) into the SWIZZLE_NONE
-//               K-major core-matrix layout.
+//   warp 19     TMEM owner + tcgen05.mma issuer (M=128, N=NPAD, K=16 x 4 per k-tile).
+//               A tcgen05.mma of this shape holds the issuing thread ~45 cycles and
+//               the tensor pipe does not queue behind it, so every cycle this loop
+//               spends outside MMA issue is tensor-pipe idle time: it polls plain
+//               smem counters (not mbarriers) and syncs/commits once per PAIR of
+//               k-tiles.
 // The core-matrix layout puts element (x, y) in bank (x%8)*4 + (y%8)/2, which is
 // exactly the reference's bank_id (proj/include/tcsl/tcsl_format.hpp:18), so the
-// encoder's ahead-of-time bank reordering keeps the scatter near one wavefront
+// encoder's ahead-of-time bank reordering keeps the scatter close to one wavefront
 // per group.
 //
 // Work unit = (row block rb, k-split s): k-tiles [s*tk/S, (s+1)*tk/S).
@@ -49,26 +52,24 @@ constexpr int kMTB = 128, kKTB = 64;
 constexpr uint32_t kABytes = kMTB * kKTB * 2;  // dense fp16 tile, 16 KB
 constexpr int kTeams = 3;                      // decode teams
 constexpr int kTeamWarps = 4;                  // warps per team
-// Warp roles. The scheduler favours higher warp ids, so the MMA issuer — the
-// pacing resource — gets the highest id; decode warps take the low ids.
-constexpr int kWarpDec = 0;                                 // 12 decode warps: 0..11
-constexpr int kWarpEpi = kTeams * kTeamWarps;               // 4 epilogue warps: 12..15 (id % 4 = TMEM quarter)
-constexpr int kWarpX = kWarpEpi + 4;                        // 16: X producer
-constexpr int kWarpPf = kWarpX + 1;                         // 17: L2 prefetcher
-constexpr int kWarpMma = kWarpX + 3;                        // 19: TMEM owner + MMA issuer
+constexpr int kWarpDec = 0;                    // decode warps 0 .. 11
+constexpr int kWarpEpi = kTeams * kTeamWarps;  // epilogue warps 12 .. 15 (id % 4 = TMEM lane quarter)
+constexpr int kWarpX = kWarpEpi + 4;           // 16
+constexpr int kWarpPf = kWarpX + 1;            // 17
+constexpr int kWarpMma = kWarpX + 3;           // 19
 constexpr int kThreads = 32 * (kWarpMma + 1);
-constexpr int kChunkG = 16;                    // groups per warp per register chunk
+constexpr int kChunkG = 24;                    // groups per warp held in registers per team-tile
 constexpr int kPrefetchAhead = 24;             // k-tiles of entries kept in flight toward L2
 
 template <int NPAD>
 struct Cfg {
-  static constexpr int kBoxW = NPAD < 64 ? NPAD : 64;       // TMA box / swizzle atom width
+  static constexpr int kBoxW = NPAD < 64 ? NPAD : 64;        // TMA box / swizzle atom width
   static constexpr int kBoxes = NPAD / kBoxW;
-  static constexpr int kTX = NPAD <= 64 ? 4 : 1;             // k-tiles per X stage
+  static constexpr int kTX = NPAD <= 32 ? 4 : (NPAD == 64 ? 2 : 1);  // k-tiles per X stage
   static constexpr uint32_t kBoxBytes = 64u * kTX * kBoxW * 2;
   static constexpr uint32_t kXStage = kBoxBytes * kBoxes;
-  static constexpr int kNX = (65536 / kXStage) < 2 ? 2 : ((65536 / kXStage) > 4 ? 4 : (65536 / kXStage));
-  static constexpr int kNA = kTeams * (NPAD <= 64 ? 3 : 2);  // dense-tile buffers
+  static constexpr int kNX = (49152 / kXStage) < 2 ? 2 : ((49152 / kXStage) > 4 ? 4 : (49152 / kXStage));
+  static constexpr int kNA = NPAD <= 128 ? 10 : 8;           // dense-tile buffers (even: MMA pairs)
   static constexpr uint32_t kRowBytes = kBoxW * 2;
   static constexpr uint32_t kLayout = kRowBytes == 16 ? 0u : (kRowBytes == 32 ? 6u : (kRowBytes == 64 ? 4u : 2u));
   // SWIZZLE_NONE (NPAD=8): LBO = k-group stride (8 rows x 16 B); swizzled: SBO = 8-row
@@ -82,7 +83,7 @@ struct Cfg {
   // smem carve-up (from a 1024-aligned base)
   static constexpr uint32_t kOffX = kNA * kABytes;
   static constexpr uint32_t kOffBar = kOffX + kNX * kXStage;
-  static constexpr uint32_t kNumBars = kNA + 2 * kNX + 4;
+  static constexpr uint32_t kNumBars = kNA / 2 + 2 * kNX + 4;
   static constexpr uint32_t kOffFlags = kOffBar + 8 * kNumBars;
   static constexpr uint32_t kSmem = 1024 + kOffFlags + 4 * kNA + 16;
 };
@@ -98,14 +99,7 @@ struct Params {
   int ldo;
   int* err;
   unsigned long long* trace;  // TCSL_TRACE builds only: per-event clock64 stamps of CTA 0
-  int debug;                  // TCSL_TRACE builds only: 1 MMA ignores decode, 2 no scatter, 4 no zeroing
 };
-
-#ifdef TCSL_TRACE
-#define DBG(bit) (p.debug & (bit))
-#else
-#define DBG(bit) 0
-#endif
 
 #ifdef TCSL_TRACE
 #define TRACE(slot, idx) \
@@ -193,6 +187,43 @@ __device__ __forceinline__ void wait_counter(uint32_t addr, uint32_t target) {
   }
 }
 
+// One decode warp's share of a team-tile: E holds its first kChunkG groups
+// (loaded earlier); meanwhile F is filled with its share of the team's next tile.
+template <int NA>
+__device__ __forceinline__ void decode_tile(const Params& p, uint32_t (&E)[kChunkG], uint32_t (&F)[kChunkG],
+                                            uint32_t a_tile, uint32_t a0, uint32_t g0, uint32_t g1,
+                                            uint32_t n0, uint32_t ng0, uint32_t ng1, int lane,
+                                            uint32_t& err_or) {
+  // next team-tile's share first, so its L2 latency overlaps this tile's scatter
+  const uint32_t* nsrc = p.ent + n0 + 32 * ng0 + lane;
+  const uint32_t ncnt = ng1 - ng0;
+#pragma unroll
+  for (int jb = 0; jb < kChunkG; jb += 4) {
+    if (static_cast<uint32_t>(jb) >= ncnt) break;
+#pragma unroll
+    for (int j = jb; j < jb + 4; ++j)
+      if (static_cast<uint32_t>(j) < ncnt) F[j] = ldg_stream(nsrc + 32 * j);
+  }
+  const uint32_t cnt = g1 - g0;
+#pragma unroll
+  for (int jb = 0; jb < kChunkG; jb += 4) {
+    if (static_cast<uint32_t>(jb) >= cnt) break;
+#pragma unroll
+    for (int j = jb; j < jb + 4; ++j) {
+      if (static_cast<uint32_t>(j) < cnt) {
+        err_or |= E[j];
+        sts16(a_tile + a_offset(E[j]), E[j] >> 16);
+      }
+    }
+  }
+  // rare: more than kChunkG groups for this warp (density above ~25 %)
+  for (uint32_t g = g0 + kChunkG; g < g1; ++g) {
+    const uint32_t e = ldg_stream(p.ent + a0 + 32 * g + lane);
+    err_or |= e;
+    sts16(a_tile + a_offset(e), e >> 16);
+  }
+}
+
 template <int NPAD>
 __global__ void __launch_bounds__(kThreads, 1)
     spmm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
@@ -204,8 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t s_a = (raw + 1023u) & ~1023u;
   const uint32_t s_x = s_a + C::kOffX;
   const uint32_t s_bar = s_a + C::kOffBar;
-  const uint32_t b_aempty = s_bar;  // [NA]   MMA of the buffer's last tile complete
-  const uint32_t b_xfull = s_bar + 8 * NA, b_xempty = b_xfull + 8 * NX;
+  const uint32_t b_aempty = s_bar;  // [NA/2] MMAs of both tiles of a buffer pair complete
+  const uint32_t b_xfull = s_bar + 8 * (NA / 2), b_xempty = b_xfull + 8 * NX;
   const uint32_t b_dfull = b_xempty + 8 * NX, b_dempty = b_dfull + 16;
   const uint32_t s_flags = s_a + C::kOffFlags;  // [NA] decode-warp completions per buffer
   const uint32_t s_tmem_slot = s_flags + 4 * NA;
@@ -217,10 +248,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NA; ++i) {
-      mbar_init(b_aempty + 8 * i, 1);
-      st_shared_u32(s_flags + 4 * i, 0);
-    }
+    for (int i = 0; i < NA / 2; ++i) mbar_init(b_aempty + 8 * i, 1);
+    for (int i = 0; i < NA; ++i) st_shared_u32(s_flags + 4 * i, 0);
     for (int i = 0; i < NX; ++i) {
       mbar_init(b_xfull + 8 * i, 1);
       mbar_init(b_xempty + 8 * i, 1);
@@ -266,6 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // registers); one elected lane issues. Descriptors are base + byte offset/16.
     const uint64_t a_desc0 = smem_desc(s_a, 128, 1024, 0);
     const uint64_t b_desc0 = smem_desc(s_x, C::kLBO, C::kSBO, C::kLayout);
+    uint32_t total = 0;  // k-tiles of this CTA
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const Unit un = unit_of(p, u);
+      total += un.kt1 - un.kt0;
+    }
     uint32_t gt = 0, ui = 0, gs = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
       const Unit un = unit_of(p, u);
@@ -278,10 +312,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t xs = gs % NX;
         if (in_stage == 0) mbar_wait(b_xfull + 8 * xs, (gs / NX) & 1);
         const uint32_t b = gt % NA;
-        if (lane == 0) TRACE(5, gt);
-        if (!DBG(1)) wait_counter(s_flags + 4 * b, kTeamWarps * (gt / NA + 1));
-        if (lane == 0) TRACE(6, gt);
-        tc_fence_after();
+        if ((gt & 1u) == 0) {
+          // both tiles of the pair decoded? (one sync point per two k-tiles)
+          if (lane == 0) TRACE(5, gt);
+          wait_counter(s_flags + 4 * b, kTeamWarps * (gt / NA + 1));
+          if (gt + 1 < total) wait_counter(s_flags + 4 * (b + 1), kTeamWarps * ((gt + 1) / NA + 1));
+          if (lane == 0) TRACE(6, gt);
+          tc_fence_after();
+        }
         const uint64_t ad = a_desc0 + ((b * kABytes) >> 4);
         const uint64_t bd = b_desc0 + ((xs * C::kXStage + in_stage * C::kTileStep) >> 4);
         if (elect_one()) {
@@ -289,13 +327,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int s = 0; s < kKTB / 16; ++s)
             mma_f16_ss(d_tmem, ad + (s * 256 >> 4), bd + (s * C::kKStep >> 4), C::kIdesc,
                        (kt > un.kt0 || s > 0) ? 1u : 0u);
-          mma_commit(b_aempty + 8 * b);
+          if ((gt & 1u) || gt + 1 == total) mma_commit(b_aempty + 8 * (b >> 1));
           if (in_stage == C::kTX - 1 || kt + 1 == un.kt1) mma_commit(b_xempty + 8 * xs);
-          *progress = gt + 1;
+          if ((gt & 3u) == 3u) *progress = gt + 1;
         }
         __syncwarp();
         if (in_stage == C::kTX - 1 || kt + 1 == un.kt1) ++gs;
-        if (lane == 0) TRACE(7, gt);
+        if (lane == 0 && (gt & 1u)) TRACE(7, gt - 1);
       }
       if (elect_one()) mma_commit(b_dfull + 8 * acc);
       __syncwarp();
@@ -375,9 +413,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= kWarpDec && warp < kWarpDec + kTeams * kTeamWarps) {
     // ---------------------------------------------------------------- decode teams
     // Team t owns the k-tiles gt = t, t + kTeams, ...; each of its 4 warps owns a
-    // contiguous quarter of the tile's groups. Entry loads run one register chunk
-    // ahead across team-tiles and offsets two team-tiles ahead, so L2 latency
-    // stays off the critical path.
+    // contiguous quarter of the tile's groups. Two register sets alternate
+    // between team-tiles (no copies): while one tile is scattered, the next
+    // team-tile's entries are in flight; offsets run two team-tiles ahead.
     const int dw = warp - kWarpDec;
     const int team = dw / kTeamWarps;
     const int tw = dw % kTeamWarps;
@@ -387,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t err_or = 0;
     bool bad_off = false;
     uint32_t a0 = 0, a1 = 0, n0 = 0, n1 = 0;
-    uint32_t e[kChunkG];
+    uint32_t E0[kChunkG], E1[kChunkG];
     bool has_n = false;
     if (more) {
       a0 = __ldg(p.off + w.t);
@@ -396,13 +434,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t g0 = ng * tw / kTeamWarps, g1 = ng * (tw + 1) / kTeamWarps;
 #pragma unroll
       for (int j = 0; j < kChunkG; ++j)
-        e[j] = (g0 + j < g1) ? ldg_stream(p.ent + a0 + 32 * (g0 + j) + lane) : 0u;
+        if (g0 + j < g1) E0[j] = ldg_stream(p.ent + a0 + 32 * (g0 + j) + lane);
       has_n = w.advance(p, kTeams);
       if (has_n) {
         n0 = __ldg(p.off + w.t);
         n1 = __ldg(p.off + w.t + 1);
       }
     }
+    int parity = 0;  // which register set holds the current tile
     while (more) {
       const uint32_t ng = tile_groups(p, a0, a1);
       if (a1 != a0 + 32 * ng) bad_off = true;
@@ -421,8 +460,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t use = gt / NA;
       const uint32_t a_tile = s_a + b * kABytes;
       if (tw == 0 && lane == 0) TRACE(0, gt);
-      if (use > 0 && !DBG(4)) {
-        mbar_wait(b_aempty + 8 * b, (use - 1) & 1);
+      if (use > 0) {
+        mbar_wait(b_aempty + 8 * (b >> 1), (use - 1) & 1);
         const uint32_t q0 = a_tile + tw * (kABytes / kTeamWarps);
 #pragma unroll
         for (int r = 0; r < static_cast<int>(kABytes / kTeamWarps / 512); ++r) sts128_zero(q0 + 512 * r + 16 * lane);
@@ -430,32 +469,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tw == 0 && lane == 0) TRACE(1, gt);
       named_bar_sync(1 + team, kTeamWarps * 32);
       if (tw == 0 && lane == 0) TRACE(2, gt);
-      uint32_t c0 = g0;
-      do {
-        // the chunk after this one: rest of my quarter, else my quarter of the next team-tile
-        uint32_t f[kChunkG];
-        const bool same = c0 + kChunkG < g1;
-        const uint32_t* fsrc = same ? p.ent + a0 + 32 * (c0 + kChunkG) + lane : p.ent + n0 + 32 * ng0 + lane;
-        const uint32_t fcnt = same ? g1 - c0 - kChunkG : ng1 - ng0;
-#pragma unroll
-        for (int j = 0; j < kChunkG; ++j) f[j] = (static_cast<uint32_t>(j) < fcnt) ? ldg_stream(fsrc + 32 * j) : 0u;
-        const uint32_t cnt = g1 - c0;  // may exceed kChunkG; only the first kChunkG are in e[]
-#pragma unroll
-        for (int j = 0; j < kChunkG; ++j) {
-          if (static_cast<uint32_t>(j) < cnt && !DBG(2)) {
-            err_or |= e[j];
-            sts16(a_tile + a_offset(e[j]), e[j] >> 16);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < kChunkG; ++j) e[j] = f[j];
-        c0 += kChunkG;
-      } while (c0 < g1);
+      if (parity == 0)
+        decode_tile<NA>(p, E0, E1, a_tile, a0, g0, g1, n0, ng0, ng1, lane, err_or);
+      else
+        decode_tile<NA>(p, E1, E0, a_tile, a0, g0, g1, n0, ng0, ng1, lane, err_or);
       if (tw == 0 && lane == 0) TRACE(3, gt);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) red_release_smem_add(s_flags + 4 * b, 1u);
       if (tw == 0 && lane == 0) TRACE(4, gt);
+      parity ^= 1;
       more = has_n;
       a0 = n0;
       a1 = n1;
@@ -595,14 +618,11 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
   p.ldo = plan.n;
   p.err = err;
   p.trace = g_trace;
-#ifdef TCSL_TRACE
-  p.debug = getenv("TCSL_DEBUG") ? atoi(getenv("TCSL_DEBUG")) : 0;
-#endif
   // Column slabs of <= 256 (one TMEM accumulator pair each).
   for (int col0 = 0; col0 < plan.n; col0 += 256) {
     const int n_pad = pad_n(std::min(256, plan.n - col0));
     const int box_w = std::min(n_pad, 64);
-    const int box_rows = n_pad <= 64 ? 256 : 64;  // Cfg<NPAD>::kTX k-tiles per stage
+    const int box_rows = 64 * (n_pad <= 32 ? 4 : (n_pad == 64 ? 2 : 1));  // Cfg<NPAD>::kTX k-tiles per stage
     p.col0 = col0;
     const uint32_t row_bytes = box_w * 2;
     const CUtensorMapSwizzle swz =
