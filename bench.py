@@ -127,16 +127,18 @@ def run_ours(args, rank, world):
     hbm_peak, tc_peak, peak_kind = peaks()
 
     # ---- setup: synthetic weights generated + encoded on the GPU (row shard per rank)
-    mats = {}
+    from paper_2309_10285_b200.sharding import shard_plan
+
+    mats, plans = {}, {}
     for name, beta, n in cells:
         if (name, beta) in mats:
             continue
         M, K = SHAPES[name]
-        tm = -(-M // 128)
-        tr0, tr1 = tm * rank // world, tm * (rank + 1) // world
-        rows = min(M, tr1 * 128) - tr0 * 128
-        w = tc.gen_synthetic(rows, K, beta, seed=hash((name, beta, rank)) & 0xFFFFFFFF)
-        mats[(name, beta)] = (tc.encode(w), tr0 * 128, rows)
+        plan = shard_plan(M, 128, world)
+        sh = plan[rank]
+        w = tc.gen_synthetic(max(sh.rows, 1), K, beta, seed=hash((name, beta, rank)) & 0xFFFFFFFF)
+        mats[(name, beta)] = (tc.encode(w), sh.row0, sh.rows)
+        plans[(name, beta)] = plan
         del w
     torch.cuda.synchronize()
     xs, ys, gathered, wss = {}, {}, {}, {}
@@ -145,21 +147,23 @@ def run_ours(args, rank, world):
         if (K, n) not in xs:
             xs[(K, n)] = tc.gen_synthetic(K, n, 0.0, seed=K * 131 + n)
         t, r0, rows = mats[(name, beta)]
-        ys[(name, beta, n)] = torch.empty((rows, n), dtype=torch.float32, device=dev)
+        ys[(name, beta, n)] = torch.empty((t.m, n), dtype=torch.float32, device=dev)
         wss[(name, beta, n)] = tc.SpmmWorkspace()
         if world > 1:
-            maxrows = max(min(M, -(-M // 128) * (r + 1) // world * 128) - (-(-M // 128) * r // world) * 128
-                          for r in range(world))
-            gathered[(name, beta, n)] = (torch.empty((world * maxrows, n), dtype=torch.float32, device=dev),
-                                         torch.zeros((maxrows, n), dtype=torch.float32, device=dev))
+            rmax = max(s.rows for s in plans[(name, beta)])
+            gathered[(name, beta, n)] = (torch.empty((world * rmax, n), dtype=torch.float32, device=dev),
+                                         torch.zeros((rmax, n), dtype=torch.float32, device=dev))
 
     def one_cell(name, beta, n):
+        # row-sharded SpMM (paper_2309_10285_b200.sharding): local rows, then one
+        # NCCL all-gather of the padded row shards (buffers preallocated so the
+        # whole step can be captured in a CUDA graph)
         t, r0, rows = mats[(name, beta)]
         y = ys[(name, beta, n)]
         tc.spmm(t, xs[(SHAPES[name][1], n)], out=y, ws=wss[(name, beta, n)], check=False)
         if world > 1:
             full, pad = gathered[(name, beta, n)]
-            pad[:rows].copy_(y)
+            pad[:rows].copy_(y[:rows])
             dist.all_gather_into_tensor(full, pad)
 
     def step():

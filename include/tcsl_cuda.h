@@ -107,6 +107,17 @@ int tcsl_cuda_spmm_exact(const uint32_t* dOffsets, const uint32_t* dEntries, uin
 int tcsl_cuda_rebase_offsets(const uint32_t* dOffsets, uint32_t tile0, uint32_t tile1, uint32_t* dOut,
                              void* stream);
 
+/* ------------------------------------------------------- memory plumbing */
+/* Thin wrappers so host bindings (C++, ctypes, cgo, JNI) never link a CUDA
+ * runtime of their own. Same semantics as the CUDA runtime calls. */
+int tcsl_cuda_malloc(void** dptr, size_t bytes);
+int tcsl_cuda_free(void* dptr);
+int tcsl_cuda_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+int tcsl_cuda_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
+int tcsl_cuda_memset(void* dptr, int value, size_t bytes, void* stream);
+int tcsl_cuda_stream_sync(void* stream);
+int tcsl_cuda_device_count(int* count);
+
 /* -------------------------------------------------------- bench utilities */
 /* Synthetic random-sparse binary16 weights: each element is +0.0 with
  * probability beta, else a value with the reference's value law (uniform

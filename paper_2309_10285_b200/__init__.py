@@ -90,6 +90,13 @@ def lib() -> C.CDLL:
         "tcsl_cuda_spmm_exact": ([vp, vp, u64, u32, u32, i32, i32, vp, i32, vp, vp, sz, vp, vp], i32),
         "tcsl_cuda_rebase_offsets": ([vp, u32, u32, vp, vp], i32),
         "tcsl_cuda_gen_synthetic": ([vp, u64, C.c_double, u64, vp], i32),
+        "tcsl_cuda_malloc": ([C.POINTER(vp), sz], i32),
+        "tcsl_cuda_free": ([vp], i32),
+        "tcsl_cuda_memcpy_h2d": ([vp, vp, sz, vp], i32),
+        "tcsl_cuda_memcpy_d2h": ([vp, vp, sz, vp], i32),
+        "tcsl_cuda_memset": ([vp, i32, sz, vp], i32),
+        "tcsl_cuda_stream_sync": ([vp], i32),
+        "tcsl_cuda_device_count": ([C.POINTER(i32)], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -104,7 +111,9 @@ EXPORTED_SYMBOLS = [
     "tcsl_cuda_encode_workspace", "tcsl_cuda_encode_count", "tcsl_cuda_encode_emit", "tcsl_cuda_decode",
     "tcsl_cuda_validate", "tcsl_cuda_spmm_workspace", "tcsl_cuda_spmm", "tcsl_cuda_spmm_auto_split",
     "tcsl_cuda_splitk_reduce", "tcsl_cuda_spmm_exact_workspace", "tcsl_cuda_spmm_exact",
-    "tcsl_cuda_rebase_offsets", "tcsl_cuda_gen_synthetic",
+    "tcsl_cuda_rebase_offsets", "tcsl_cuda_gen_synthetic", "tcsl_cuda_malloc", "tcsl_cuda_free",
+    "tcsl_cuda_memcpy_h2d", "tcsl_cuda_memcpy_d2h", "tcsl_cuda_memset", "tcsl_cuda_stream_sync",
+    "tcsl_cuda_device_count",
 ]
 
 

@@ -230,6 +230,39 @@ int tcsl_cuda_rebase_offsets(const uint32_t* dOffsets, uint32_t tile0, uint32_t 
   return cuda_status(tcslk::launch_rebase(dOffsets, tile0, tile1, dOut, static_cast<cudaStream_t>(stream)));
 }
 
+// ---------------------------------------------------------- memory plumbing
+int tcsl_cuda_malloc(void** dptr, size_t bytes) {
+  if (!dptr) return TCSL_STATUS_INVALID_ARGUMENT;
+  *dptr = nullptr;
+  return bytes ? cuda_status(cudaMalloc(dptr, bytes)) : TCSL_STATUS_OK;
+}
+int tcsl_cuda_free(void* dptr) { return dptr ? cuda_status(cudaFree(dptr)) : TCSL_STATUS_OK; }
+int tcsl_cuda_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
+  if (!bytes) return TCSL_STATUS_OK;
+  return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)));
+}
+int tcsl_cuda_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
+  if (!bytes) return TCSL_STATUS_OK;
+  return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
+}
+int tcsl_cuda_memset(void* dptr, int value, size_t bytes, void* stream) {
+  if (!bytes) return TCSL_STATUS_OK;
+  return cuda_status(cudaMemsetAsync(dptr, value, bytes, static_cast<cudaStream_t>(stream)));
+}
+int tcsl_cuda_stream_sync(void* stream) {
+  return cuda_status(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+}
+int tcsl_cuda_device_count(int* count) {
+  if (!count) return TCSL_STATUS_INVALID_ARGUMENT;
+  *count = 0;
+  const cudaError_t e = cudaGetDeviceCount(count);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+    *count = 0;
+    return TCSL_STATUS_OK;
+  }
+  return cuda_status(e);
+}
+
 int tcsl_cuda_gen_synthetic(uint16_t* dW, uint64_t count, double beta, uint64_t seed, void* stream) {
   if (!dW || !(beta >= 0.0 && beta <= 1.0)) return TCSL_STATUS_INVALID_ARGUMENT;
   return cuda_status(tcslk::launch_gen_synthetic(dW, count, beta, seed, static_cast<cudaStream_t>(stream)));

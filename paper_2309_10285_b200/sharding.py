@@ -1,0 +1,95 @@
+"""Row (M) sharding of one Tiled-CSL weight across the GPUs of a node
+(BASELINE.json north_star (4)).
+
+A shard is the contiguous range of tile rows [tr0, tr1): because tiles are
+stored row-major over the tile grid (proj/src/tcsl_format.cpp:56-57), its
+tiles are the contiguous range [tr0*tk, tr1*tk) and its entries the contiguous
+range [off[tr0*tk], off[tr1*tk]); rebasing the offsets gives exactly the
+Tiled-CSL that `encode` would produce for those rows (checked in the tests).
+X is replicated; each rank computes its rows of Y, and one all-gather (NCCL
+over NVLink on GPUs, gloo on CPU) assembles Y in rank order. No other
+collective exists on this path.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    tr0: int      # first tile row
+    tr1: int      # one past the last tile row
+    row0: int     # first matrix row
+    rows: int     # rows in this shard (the last one may be ragged)
+
+
+def shard_plan(m: int, m_tb: int, world: int) -> list[Shard]:
+    """Balanced contiguous tile-row ranges, one per rank (empty ranges allowed)."""
+    tiles_m = -(-m // m_tb)
+    out = []
+    for r in range(world):
+        tr0, tr1 = tiles_m * r // world, tiles_m * (r + 1) // world
+        row0 = tr0 * m_tb
+        rows = max(0, min(m, tr1 * m_tb) - row0)
+        out.append(Shard(r, tr0, tr1, row0, rows))
+    return out
+
+
+def slice_rows(offsets: np.ndarray, entries: np.ndarray, tiles_k: int, shard: Shard):
+    """Host slice of a Tiled-CSL matrix: (rebased offsets, entry view)."""
+    t0, t1 = shard.tr0 * tiles_k, shard.tr1 * tiles_k
+    off = np.asarray(offsets, dtype=np.uint32)[t0:t1 + 1]
+    lo, hi = int(off[0]), int(off[-1])
+    return (off - off[0]).astype(np.uint32), np.asarray(entries, dtype=np.uint32)[lo:hi]
+
+
+def max_rows(plan: list[Shard]) -> int:
+    return max(s.rows for s in plan)
+
+
+def allgather_rows(y_local, plan: list[Shard], group=None):
+    """All-gather row shards of Y (torch tensors, [rows_r, n]) into the full Y.
+
+    Shards are padded to the largest shard so a single all_gather_into_tensor
+    (one NCCL call) moves everything; padding rows are dropped afterwards."""
+    import torch
+    import torch.distributed as dist
+
+    world = len(plan)
+    n = y_local.shape[1]
+    rmax = max_rows(plan)
+    pad = torch.zeros((rmax, n), dtype=y_local.dtype, device=y_local.device)
+    pad[: y_local.shape[0]].copy_(y_local)
+    full = torch.empty((world * rmax, n), dtype=y_local.dtype, device=y_local.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(full, pad, group=group)
+    else:
+        dist.all_gather(list(full.chunk(world)), pad, group=group)
+    parts = [full[s.rank * rmax: s.rank * rmax + s.rows] for s in plan]
+    return torch.cat(parts, dim=0)
+
+
+class RowShardedSpmm:
+    """One rank's part of a row-sharded SpMM on the GPU: holds the rank's
+    Tiled-CSL shard (device), runs the tcgen05 SpMM on it and all-gathers Y."""
+
+    def __init__(self, t_full, world: int, rank: int, group=None):
+        from . import shard_rows
+        self.plan = shard_plan(t_full.m, t_full.cfg.m_tb, world)
+        self.shard = self.plan[rank]
+        self.group = group
+        self.local = shard_rows(t_full, self.shard.tr0, self.shard.tr1) if self.shard.rows else None
+        self.m = t_full.m
+
+    def __call__(self, x, split_k: int = 0):
+        import torch
+
+        from . import spmm
+        if self.local is not None:
+            y = spmm(self.local, x, split_k=split_k)
+        else:
+            y = torch.empty((0, x.shape[1]), dtype=torch.float32, device=x.device)
+        return allgather_rows(y, self.plan, self.group)
