@@ -89,6 +89,15 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(static_cast<uint16_t>(v)) : "memory");
 }
+// Predicated 16-bit store: stays straight-line code (no branch around it).
+__device__ __forceinline__ void sts16_if(uint32_t addr, uint32_t v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.u32 p, %2, 0;\n\t"
+      "@p st.shared.u16 [%0], %1;\n\t}" ::"r"(addr),
+      "h"(static_cast<uint16_t>(v)), "r"(static_cast<uint32_t>(pred))
+      : "memory");
+}
 __device__ __forceinline__ void sts128_zero(uint32_t addr) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0u) : "memory");
 }

@@ -102,6 +102,15 @@ struct Params {
 };
 
 #ifdef TCSL_TRACE
+// debug-only experiment switches (env TCSL_DEBUG): 2 skip scatter, 4 skip zeroing,
+// 32 skip entry loads
+__constant__ int c_debug;
+#define DBG(bit) (c_debug & (bit))
+#else
+#define DBG(bit) 0
+#endif
+
+#ifdef TCSL_TRACE
 #define TRACE(slot, idx) \
   do { if (blockIdx.x == 0 && p.trace && (idx) < 4096) p.trace[(slot) * 4096 + (idx)] = clock64(); } while (0)
 #else
@@ -194,26 +203,30 @@ __device__ __forceinline__ void decode_tile(const Params& p, uint32_t (&E)[kChun
                                             uint32_t a_tile, uint32_t a0, uint32_t g0, uint32_t g1,
                                             uint32_t n0, uint32_t ng0, uint32_t ng1, int lane,
                                             uint32_t& err_or) {
-  // next team-tile's share first, so its L2 latency overlaps this tile's scatter
-  const uint32_t* nsrc = p.ent + n0 + 32 * ng0 + lane;
+  // Straight-line code in blocks of 8 groups: loads are unconditional (clamped to
+  // the last valid group), stores predicated in PTX — no per-group branches.
+  // Next team-tile's share first, so its L2 latency overlaps this tile's scatter.
   const uint32_t ncnt = ng1 - ng0;
+  if (ncnt) {
+    const uint32_t* nsrc = p.ent + n0 + 32 * ng0 + lane;
+    const uint32_t last = ncnt - 1;
 #pragma unroll
-  for (int jb = 0; jb < kChunkG; jb += 4) {
-    if (static_cast<uint32_t>(jb) >= ncnt) break;
+    for (int jb = 0; jb < kChunkG; jb += 8) {
+      if (static_cast<uint32_t>(jb) >= ncnt) break;
 #pragma unroll
-    for (int j = jb; j < jb + 4; ++j)
-      if (static_cast<uint32_t>(j) < ncnt) F[j] = ldg_stream(nsrc + 32 * j);
+      for (int j = jb; j < jb + 8; ++j)
+        if (!DBG(32)) F[j] = ldg_stream(nsrc + 32 * min(static_cast<uint32_t>(j), last));
+    }
   }
   const uint32_t cnt = g1 - g0;
 #pragma unroll
-  for (int jb = 0; jb < kChunkG; jb += 4) {
+  for (int jb = 0; jb < kChunkG; jb += 8) {
     if (static_cast<uint32_t>(jb) >= cnt) break;
 #pragma unroll
-    for (int j = jb; j < jb + 4; ++j) {
-      if (static_cast<uint32_t>(j) < cnt) {
-        err_or |= E[j];
-        sts16(a_tile + a_offset(E[j]), E[j] >> 16);
-      }
+    for (int j = jb; j < jb + 8; ++j) {
+      // slots past cnt hold duplicates of valid entries (or zeros): harmless for err_or
+      err_or |= E[j];
+      sts16_if(a_tile + a_offset(E[j]), E[j] >> 16, static_cast<uint32_t>(j) < cnt && !DBG(2));
     }
   }
   // rare: more than kChunkG groups for this warp (density above ~25 %)
@@ -426,6 +439,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool bad_off = false;
     uint32_t a0 = 0, a1 = 0, n0 = 0, n1 = 0;
     uint32_t E0[kChunkG], E1[kChunkG];
+#pragma unroll
+    for (int j = 0; j < kChunkG; ++j) E0[j] = E1[j] = 0u;  // unused slots must not look like bad locations
     bool has_n = false;
     if (more) {
       a0 = __ldg(p.off + w.t);
@@ -461,22 +476,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t a_tile = s_a + b * kABytes;
       if (tw == 0 && lane == 0) TRACE(0, gt);
       if (use > 0) {
-        mbar_wait(b_aempty + 8 * (b >> 1), (use - 1) & 1);
+        // sleep in hardware: spinning try_waits from 12 warps starve the tcgen05 issue path
+        mbar_wait_sleep(b_aempty + 8 * (b >> 1), (use - 1) & 1);
         const uint32_t q0 = a_tile + tw * (kABytes / kTeamWarps);
 #pragma unroll
-        for (int r = 0; r < static_cast<int>(kABytes / kTeamWarps / 512); ++r) sts128_zero(q0 + 512 * r + 16 * lane);
+        for (int r = 0; r < static_cast<int>(kABytes / kTeamWarps / 512); ++r)
+          if (!DBG(4)) sts128_zero(q0 + 512 * r + 16 * lane);
       }
       if (tw == 0 && lane == 0) TRACE(1, gt);
       named_bar_sync(1 + team, kTeamWarps * 32);
       if (tw == 0 && lane == 0) TRACE(2, gt);
-      if (parity == 0)
+      if (DBG(1024)) {
+      } else if (parity == 0)
         decode_tile<NA>(p, E0, E1, a_tile, a0, g0, g1, n0, ng0, ng1, lane, err_or);
       else
         decode_tile<NA>(p, E1, E0, a_tile, a0, g0, g1, n0, ng0, ng1, lane, err_or);
       if (tw == 0 && lane == 0) TRACE(3, gt);
-      fence_proxy_async_smem();
+      if (!DBG(64)) fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) red_release_smem_add(s_flags + 4 * b, 1u);
+      if (lane == 0) {
+        if (DBG(128))
+          asm volatile("red.relaxed.cta.shared::cta.add.u32 [%0], %1;" ::"r"(s_flags + 4 * b), "r"(1u) : "memory");
+        else
+          red_release_smem_add(s_flags + 4 * b, 1u);
+      }
       if (tw == 0 && lane == 0) TRACE(4, gt);
       parity ^= 1;
       more = has_n;
@@ -618,6 +641,12 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
   p.ldo = plan.n;
   p.err = err;
   p.trace = g_trace;
+#ifdef TCSL_TRACE
+  {
+    const int dbg = getenv("TCSL_DEBUG") ? atoi(getenv("TCSL_DEBUG")) : 0;
+    cudaMemcpyToSymbolAsync(c_debug, &dbg, sizeof dbg, 0, cudaMemcpyHostToDevice, s);
+  }
+#endif
   // Column slabs of <= 256 (one TMEM accumulator pair each).
   for (int col0 = 0; col0 < plan.n; col0 += 256) {
     const int n_pad = pad_n(std::min(256, plan.n - col0));

@@ -134,6 +134,36 @@ __global__ void bench(int iters, unsigned long long* out) {
       }
     }
     __syncthreads();
+  } else if (MODE == 10 || MODE == 11) {
+    // production-like issue loop: last warp of a 640-thread CTA, whole warp walks,
+    // elect_one issues; MODE 11 also commits + polls an smem flag per tile pair
+    if (warp == (int)(blockDim.x / 32) - 1) {
+      const uint32_t idesc = idesc_f16_f32(128, N, 1);
+      const uint64_t a_desc0 = smem_desc(sa, 128, 1024, 0);
+      const uint64_t b_desc0 = smem_desc(sb, 8192, b_sbo, b_layout);
+      for (int it = 0; it < iters; ++it) {
+        const uint64_t ad = a_desc0 + (((it & 3) * 16384) >> 4);
+        if (MODE == 11 && (it & 1) == 0) {
+          uint32_t v;
+          asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&st_flag_done)) : "memory");
+          if (v == 12345) __trap();
+          tc_fence_after();
+        }
+        if (elect_one()) {
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            mma_f16_ss(tmem + 16, ad + (s * 256 >> 4), b_desc0 + (s * 16 * b_row >> 4), idesc, (it | s) ? 1u : 0u);
+          if (MODE == 11 && (it & 1)) mma_commit(bar + 8);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) {
+        mma_commit(bar);
+      }
+      __syncwarp();
+      mbar_wait(bar, 0);
+    }
+    __syncthreads();
   } else if (threadIdx.x == 0) {
     constexpr uint32_t M = MODE == 1 ? 64 : 128;  // MODE 9 behaves like MODE 0 on random data
     const uint32_t idesc = idesc_f16_f32(M, N, 1);
@@ -173,8 +203,9 @@ void run(const char* name) {
   const int smem = 5 * 16384 + 2048;
   cudaFuncSetAttribute(bench<MODE, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 4096;
-  bench<MODE, N><<<148, 128, smem>>>(iters, d);
-  bench<MODE, N><<<148, 128, smem>>>(iters, d);
+  const int threads = MODE >= 10 && MODE <= 11 ? 640 : 128;
+  bench<MODE, N><<<148, threads, smem>>>(iters, d);
+  bench<MODE, N><<<148, threads, smem>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[148];
   cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
@@ -195,6 +226,8 @@ int main() {
   run<5, 32>("SS M=128, 2 issuing warps");
   run<6, 32>("SS M=128, 4 issuing warps");
   run<5, 16>("SS M=128, 2 issuing warps");
+  run<10, 16>("640 thr, warp 19, elect");
+  run<11, 16>("640 thr, warp 19, +flag+commit");
   run<9, 16>("SS random data");
   run<9, 64>("SS random data");
   run<7, 16>("SS + 3 warps STS.128 stream");
