@@ -59,7 +59,8 @@ constexpr int kWarpPf = kWarpX + 1;            // 17
 constexpr int kWarpMma = kWarpX + 3;           // 19
 constexpr int kThreads = 32 * (kWarpMma + 1);
 constexpr int kChunkG = 24;                    // groups per warp held in registers per team-tile
-constexpr int kPrefetchAhead = 24;             // k-tiles of entries kept in flight toward L2
+constexpr int kPrefetchAhead = 32;             // k-tiles of entries kept in flight toward L2
+constexpr int kPfChunk = 4;                    // k-tiles per L2 prefetch
 
 template <int NPAD>
 struct Cfg {
@@ -355,18 +356,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------------------------------------------------------- L2 prefetcher
     // Keeps the entry spans of the next kPrefetchAhead k-tiles on their way to
     // L2 so the decode warps' loads hit L2 instead of waiting on HBM.
-    if (lane == 0) {
-      TileWalk w;
-      uint32_t issued = 0;
-      bool more = w.start(p);
-      while (more) {
-        while (issued >= *progress + kPrefetchAhead) __nanosleep(256);
-        const uint32_t a0 = __ldg(p.off + w.t), a1 = __ldg(p.off + w.t + 1);
-        const uint32_t ng = tile_groups(p, a0, a1);
-        if (ng) bulk_prefetch_l2(p.ent + a0, ng * 128u);
-        ++issued;
-        more = w.advance(p, 1);
+    // A unit's tiles are contiguous in the entry array, so the warp prefetches
+    // chunks of kPfChunk tiles; each lane loads the bounds of one chunk (32
+    // chunks per offset round trip) and the chunks are issued in order, paced.
+    uint32_t base = 0;  // schedule index of the unit's first k-tile
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const Unit un = unit_of(p, u);
+      const uint32_t t0 = static_cast<uint32_t>(un.rb) * p.tiles_k + un.kt0;
+      const uint32_t nt = un.kt1 - un.kt0;
+      for (uint32_t c = 0; c < nt; c += 32 * kPfChunk) {
+        const uint32_t my0 = min(c + lane * kPfChunk, nt), my1 = min(my0 + kPfChunk, nt);
+        uint32_t lo = 0, hi = 0;
+        if (my1 > my0) {
+          lo = __ldg(p.off + t0 + my0);
+          hi = __ldg(p.off + t0 + my1);
+        }
+        const bool ok = hi > lo && hi <= p.n_entries && (lo & 3u) == 0;
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t first = c + i * kPfChunk;
+          if (first >= nt) break;
+          if (lane == 0)
+            while (base + first >= *progress + kPrefetchAhead) __nanosleep(64);
+          __syncwarp();
+          if (lane == i && ok) bulk_prefetch_l2(p.ent + lo, ((hi - lo) * 4u) & ~15u);
+        }
       }
+      base += nt;
     }
   } else if (warp >= kWarpEpi && warp < kWarpEpi + 4) {
     // ---------------------------------------------------------------- epilogue

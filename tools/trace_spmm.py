@@ -15,6 +15,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2309_10285_b200 as tc  # noqa: E402
 
 tc.LIB_PATH = os.path.join(tc.LIB_DIR, "libtcsl_cuda_trace.so")
+if not os.path.exists(tc.LIB_PATH):
+    import subprocess
+    subprocess.run(["nvcc", *tc.NVCC_FLAGS, "-DTCSL_TRACE", "-o", tc.LIB_PATH,
+                    *[os.path.join(tc.CSRC, f) for f in tc.SOURCES]], check=True)
 L = tc.lib()
 L.tcsl_cuda_debug_set_trace.argtypes = [C.c_void_p]
 
