@@ -38,9 +38,16 @@ bool is_default_tile(int m_tb, int k_tb) { return m_tb == 128 && k_tb == 64; }
 // Row pitch (elements) the tensor-core path uses for X: TMA wants 16-B rows.
 int x_pitch(int n) { return (n + 7) / 8 * 8; }
 
+// The split the kernel will run: the request (or the heuristic's choice),
+// clamped by the plan (at most tiles_k splits, bounded units per CTA pair).
+int planned_split(uint32_t m, uint32_t k, int n, int split) {
+  tcslk::SpmmPlan plan;
+  tcslk::spmm_sm100_plan(m, k, n, split, &plan);
+  return plan.split;
+}
+
 int effective_split(uint32_t m, uint32_t k, int n, int split_k) {
-  const int tiles_k = tcslk::div_up_i(k, 64);
-  if (split_k > 0) return split_k < tiles_k ? split_k : tiles_k;
+  if (split_k > 0) return planned_split(m, k, n, split_k);
   // the heuristic simulates the persistent schedule; memoise it per shape
   static std::mutex mu;
   static std::map<std::tuple<uint32_t, uint32_t, int>, int> cache;
@@ -48,7 +55,7 @@ int effective_split(uint32_t m, uint32_t k, int n, int split_k) {
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  const int s = tcslk::auto_split(m, k, n, 0.2 * 8192);
+  const int s = planned_split(m, k, n, tcslk::auto_split(m, k, n, 0.2 * 8192));
   cache.emplace(key, s);
   return s;
 }

@@ -3,35 +3,39 @@
 // Reference semantics: tcsl::spmm, proj/src/engine.cpp:27-78 — per 128-row
 // block, per 64-column k-tile: rebuild the dense tile from its Tiled-CSL
 // entries (extract_tile, engine.cpp:8-25) and run a dense product over every
-// element, zeros included. Here the dense product is a tcgen05 MMA with an
-// fp32 accumulator in TMEM; the reference's serial fp32 add order is not
-// reproduced (tolerance per BASELINE.json north_star), see spmm_exact for the
-// bit-exact CUDA-core mode.
+// element, zeros included. Here the dense product is a tcgen05 MMA with fp32
+// accumulators in TMEM; the reference's serial fp32 add order is not
+// reproduced (tolerance per BASELINE.json north_star; spmm_exact is the
+// bit-exact CUDA-core mode).
 //
-// One persistent CTA per SM, warp-specialised (640 threads). The scheduler
-// favours higher warp ids, so the pacing role gets the highest id:
-//   warps 0-11  decode, three teams of 4 warps on k-tiles gt % 3 == team: zero the
-//               dense tile, then each warp scatters its contiguous share of the
-//               tile's 32-entry groups (one entry per lane, loaded from L2 straight
-//               into registers one team-tile ahead) into the SWIZZLE_NONE K-major
-//               core-matrix layout
-//   warps 12-15 epilogue: tcgen05.ld accumulator -> fp32 Y rows (or split-K partials)
-//   warp 16     X producer: TMA-loads kTX k-tiles x NPAD activations per stage
-//               (MN-major, hardware swizzle = 2*NPAD bytes)
-//   warp 17     L2 prefetcher: cp.async.bulk.prefetch.L2 of the entry spans of the
-//               next kPrefetchAhead k-tiles, paced by the MMA's progress
-//   warp 19     TMEM owner + tcgen05.mma issuer (M=128, N=NPAD, K=16 x 4 per k-tile).
-//               A tcgen05.mma of this shape holds the issuing thread ~45 cycles and
-//               the tensor pipe does not queue behind it, so every cycle this loop
-//               spends outside MMA issue is tensor-pipe idle time: it polls plain
-//               smem counters (not mbarriers) and syncs/commits once per PAIR of
-//               k-tiles.
-// The core-matrix layout puts element (x, y) in bank (x%8)*4 + (y%8)/2, which is
-// exactly the reference's bank_id (proj/include/tcsl/tcsl_format.hpp:18), so the
-// encoder's ahead-of-time bank reordering keeps the scatter close to one wavefront
-// per group.
+// CTA pairs. A tcgen05.mma of M=128 x N<=64 x K=16 occupies the tensor pipe for
+// ~45 cycles whatever N is (profiles/r01_mma_bench*.txt), so one SM cannot
+// consume a 128x64 tile faster than ~180 cycles. A cluster of two CTAs on one
+// TPC issues cta_group::2 MMAs (M=256: each CTA contributes its own 128-row
+// tile, B is split by columns across the pair) at the same ~45 cycles per
+// instruction, i.e. ~91 cycles per tile per SM. The pair works on row blocks
+// 2*rp and 2*rp+1 of the same k-range in lock step.
 //
-// Work unit = (row block rb, k-split s): k-tiles [s*tk/S, (s+1)*tk/S).
+// Per CTA (608 threads), warp-specialised:
+//   warps 0-11  decode: three teams of four warps; team j owns A buffers j and
+//               j+3 and decodes the k-tiles gt = j (mod 3). Per tile each warp
+//               (1) loads its quarter of the tile's 32-entry groups from the smem
+//               entry ring (one LDS per group, conflict-free), (2) once the MMA
+//               has released the buffer, stores +0 at the addresses its previous
+//               tile in that buffer wrote (kept in registers: clear-by-rescatter,
+//               no 16 KB memset), (3) after a team barrier scatters the new values
+//               into the SWIZZLE_NONE K-major core-matrix layout, whose bank
+//               function is exactly the reference's bank_id (tcsl_format.hpp:18),
+//               and (4) arrives on the pair's "A full" barrier in the even CTA.
+//   warps 12-15 epilogue: tcgen05.ld of this CTA's 128 accumulator rows -> fp32 Y
+//               (or split-K partial sums).
+//   warp 16     X producer: TMA loads of this CTA's half of the B columns.
+//   warp 17     entry-ring producer: one cp.async.bulk per k-tile (the tile's span
+//               is contiguous and 128-B aligned because counts are padded to 32,
+//               tcsl_format.cpp:103-119) into a 64 KB ring, up to 16 tiles ahead.
+//   warp 18     TMEM owner; in the even CTA also the tcgen05.mma issuer.
+//
+// Work unit = (row-block pair rp, k-split s): k-tiles [s*tk/S, (s+1)*tk/S).
 // S == 1 writes Y directly; S > 1 writes partial sums P[s] that
 // tcsl_cuda_splitk_reduce adds in ascending s (deterministic).
 #include <cuda.h>
@@ -50,43 +54,59 @@ namespace {
 
 constexpr int kMTB = 128, kKTB = 64;
 constexpr uint32_t kABytes = kMTB * kKTB * 2;  // dense fp16 tile, 16 KB
-constexpr int kTeams = 3;                      // decode teams
+constexpr int kTeams = 5;                      // decode teams
 constexpr int kTeamWarps = 4;                  // warps per team
-constexpr int kWarpDec = 0;                    // decode warps 0 .. 11
-constexpr int kWarpEpi = kTeams * kTeamWarps;  // epilogue warps 12 .. 15 (id % 4 = TMEM lane quarter)
-constexpr int kWarpX = kWarpEpi + 4;           // 16
-constexpr int kWarpPf = kWarpX + 1;            // 17
-constexpr int kWarpMma = kWarpX + 3;           // 19
-constexpr int kThreads = 32 * (kWarpMma + 1);
-constexpr int kChunkG = 24;                    // groups per warp held in registers per team-tile
-constexpr int kPrefetchAhead = 32;             // k-tiles of entries kept in flight toward L2
-constexpr int kPfChunk = 4;                    // k-tiles per L2 prefetch
+constexpr int kNA = kTeams;                    // dense-tile buffers (one per team)
+constexpr int kGMax = 20;                      // groups per warp per tile remembered for re-clearing
+constexpr int kWarpEpi = kTeams * kTeamWarps;  // epilogue warps 24 .. 27 (id % 4 = TMEM lane quarter)
+constexpr int kWarpStream = kWarpEpi + 4;      // entry stream: bulk copies only (blocking waits)
+constexpr int kWarpPoll = kWarpStream + 1;     // polling warp: tile metadata, X stages, epilogue wake-ups
+constexpr int kWarpMma = kWarpPoll + 1;
+constexpr int kThreads = 32 * (kWarpMma + 1);  // 576
+constexpr int kBarEpi = 1 + kTeams;            // named barriers 1..kTeams: teams; then 2 for epilogue wake-ups
+constexpr uint32_t kRing = 65536;              // entry ring bytes (power of two)
+constexpr uint32_t kChunk = 16384;             // bytes per bulk copy (>= 8 KB: ~7 TB/s, profiles/r01_bulk_copy_bench.txt)
+constexpr int kNR = kRing / kChunk;            // chunks in flight
+// "chunk landed" barriers: chunk k uses cfull[k % kNB]. A decoder may wait for a
+// chunk up to ~9 tiles (<= 45 chunks) past the oldest unconsumed one; with more
+// barriers than that, the barrier's previous phase is always complete, so the
+// parity test cannot alias (mbarrier parity waits only see one phase back).
+constexpr int kNB = 64;
+constexpr int kMaxUnits = 64;                  // work units per CTA (unit table size; the host caps split)
+constexpr int kMeta = 64;                      // per-tile metadata ring (stream offset, groups)
+constexpr uint32_t kSmallBytes = 3072;         // barriers + tables (see Smem)
 
-template <int NPAD>
+// NH = B columns held by each CTA of the pair (the MMA's N is 2 * NH).
+template <int NH>
 struct Cfg {
-  static constexpr int kBoxW = NPAD < 64 ? NPAD : 64;        // TMA box / swizzle atom width
-  static constexpr int kBoxes = NPAD / kBoxW;
-  static constexpr int kTX = NPAD <= 32 ? 4 : (NPAD == 64 ? 2 : 1);  // k-tiles per X stage
+  static constexpr int kN = 2 * NH;
+  static constexpr int kBoxW = NH < 64 ? NH : 64;  // TMA box / swizzle atom width
+  static constexpr int kBoxes = NH / kBoxW;
+  static constexpr int kTX = NH <= 32 ? 4 : (NH == 64 ? 2 : 1);  // k-tiles per X stage (TMA box <= 256 rows)
   static constexpr uint32_t kBoxBytes = 64u * kTX * kBoxW * 2;
   static constexpr uint32_t kXStage = kBoxBytes * kBoxes;
   static constexpr int kNX = (49152 / kXStage) < 2 ? 2 : ((49152 / kXStage) > 4 ? 4 : (49152 / kXStage));
-  static constexpr int kNA = NPAD <= 128 ? 10 : 8;           // dense-tile buffers (even: MMA pairs)
   static constexpr uint32_t kRowBytes = kBoxW * 2;
   static constexpr uint32_t kLayout = kRowBytes == 16 ? 0u : (kRowBytes == 32 ? 6u : (kRowBytes == 64 ? 4u : 2u));
-  // SWIZZLE_NONE (NPAD=8): LBO = k-group stride (8 rows x 16 B); swizzled: SBO = 8-row
-  // k-group stride, LBO = stride between 64-column atoms.
+  // SWIZZLE_NONE (16-B rows): LBO = k-group stride (8 rows x 16 B); swizzled: SBO =
+  // 8-row k-group stride, LBO = stride between 64-column atoms.
   static constexpr uint32_t kLBO = kRowBytes == 16 ? 128u : kBoxBytes;
   static constexpr uint32_t kSBO = kRowBytes == 16 ? 128u : 8u * kRowBytes;
-  static constexpr uint32_t kKStep = 16u * kRowBytes;        // 16 k-rows per MMA
-  static constexpr uint32_t kTileStep = 64u * kRowBytes;     // next k-tile inside a stage
-  static constexpr uint32_t kTmemCols = (2 * NPAD) <= 32 ? 32 : ((2 * NPAD) <= 64 ? 64 : ((2 * NPAD) <= 128 ? 128 : ((2 * NPAD) <= 256 ? 256 : 512)));
-  static constexpr uint32_t kIdesc = idesc_f16_f32(128, NPAD, 1);
-  // smem carve-up (from a 1024-aligned base)
-  static constexpr uint32_t kOffX = kNA * kABytes;
-  static constexpr uint32_t kOffBar = kOffX + kNX * kXStage;
-  static constexpr uint32_t kNumBars = kNA / 2 + 2 * kNX + 4;
-  static constexpr uint32_t kOffFlags = kOffBar + 8 * kNumBars;
-  static constexpr uint32_t kSmem = 1024 + kOffFlags + 4 * kNA + 16;
+  static constexpr uint32_t kKStep = 16u * kRowBytes;     // 16 k-rows per MMA
+  static constexpr uint32_t kTileStep = 64u * kRowBytes;  // next k-tile inside a stage
+  static constexpr uint32_t kTmemCols =
+      (2 * kN) <= 32 ? 32 : ((2 * kN) <= 64 ? 64 : ((2 * kN) <= 128 ? 128 : ((2 * kN) <= 256 ? 256 : 512)));
+  static constexpr uint32_t kIdesc = idesc_f16_f32(256, kN, 1);
+  // smem, relative to the dynamic-smem base B (1 KB past the 16 KB-aligned window
+  // start on sm_100: the driver reserves the first 1 KB): entry ring, small
+  // tables, X stages, then the dense-tile buffers at the next 16 KB-aligned
+  // address (so a tile address is base | offset, one LOP3 in the scatter).
+  static constexpr uint32_t kOffRing = 0;
+  static constexpr uint32_t kOffSmall = kRing;
+  static constexpr uint32_t kOffX = kOffSmall + kSmallBytes;  // 1 KB aligned
+  static constexpr uint32_t kEndX = kOffX + kNX * kXStage;
+  static constexpr uint32_t kOffA = ((kEndX + 1024 + 16383) & ~16383u) - 1024;  // assuming B % 16 KB == 1 KB
+  static constexpr uint32_t kSmem = kOffA + kNA * kABytes;
 };
 
 struct Params {
@@ -94,23 +114,31 @@ struct Params {
   const uint32_t* ent;
   uint64_t n_entries;
   uint32_t m, k;
-  int tiles_m, tiles_k;
+  int tiles_m, tiles_k, tiles_mp;
   int n, col0, split, units;
   float* out;
   int ldo;
   int* err;
   unsigned long long* trace;  // TCSL_TRACE builds only: per-event clock64 stamps of CTA 0
+  int dbg;                    // ablation switches (see DBG)
 };
 
-#ifdef TCSL_TRACE
-// debug-only experiment switches (env TCSL_DEBUG): 2 skip scatter, 4 skip zeroing,
-// 32 skip entry loads
-__constant__ int c_debug;
-#define DBG(bit) (c_debug & (bit))
+#if defined(TCSL_TRACE) && defined(TCSL_HEARTBEAT)
+// debug builds: per-warp heartbeat in mapped host memory (state << 24 | value),
+// readable by the host while a kernel is stuck
+__device__ unsigned* g_hb = nullptr;
+#define HB(state, v)                                                                                  \
+  do {                                                                                                \
+    if (g_hb && (threadIdx.x & 31) == 0)                                                              \
+      reinterpret_cast<volatile unsigned*>(g_hb)[blockIdx.x * 32 + (threadIdx.x >> 5)] =               \
+          (static_cast<unsigned>(state) << 24) | (static_cast<unsigned>(v) & 0xFFFFFFu);               \
+  } while (0)
 #else
-#define DBG(bit) 0
+#define HB(state, v) do { } while (0)
 #endif
-
+// Ablation switches for performance experiments (env TCSL_DEBUG, read once per
+// process; 0 in production): 1 skip scatter+clear, 2 skip MMAs, 4 skip ring loads.
+#define DBG(bit) (p.dbg & (bit))
 #ifdef TCSL_TRACE
 #define TRACE(slot, idx) \
   do { if (blockIdx.x == 0 && p.trace && (idx) < 4096) p.trace[(slot) * 4096 + (idx)] = clock64(); } while (0)
@@ -119,303 +147,314 @@ __constant__ int c_debug;
 #endif
 
 struct Unit {
-  int rb, s, kt0, kt1;
+  int rp, s, kt0, kt1;
 };
 __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
   Unit x;
-  x.rb = u / p.split;
-  x.s = u - x.rb * p.split;
+  x.rp = u / p.split;
+  x.s = u - x.rp * p.split;
   x.kt0 = static_cast<int>(static_cast<long long>(x.s) * p.tiles_k / p.split);
   x.kt1 = static_cast<int>(static_cast<long long>(x.s + 1) * p.tiles_k / p.split);
   return x;
 }
 
-// Walks this CTA's k-tiles in schedule order: (unit, kt, global tile index t).
-struct TileWalk {
-  int u, kt, kt1;
-  uint32_t t;
-  __device__ __forceinline__ bool start(const Params& p) {
-    u = blockIdx.x;
-    return load(p);
-  }
-  __device__ __forceinline__ bool load(const Params& p) {
-    if (u >= p.units) return false;
-    const Unit un = unit_of(p, u);
-    kt = un.kt0;
-    kt1 = un.kt1;
-    t = static_cast<uint32_t>(un.rb) * p.tiles_k + un.kt0;
-    return true;
-  }
-  // advance by `steps` tiles (crossing units as needed)
-  __device__ __forceinline__ bool advance(const Params& p, int steps) {
-    while (steps > 0) {
-      const int left = kt1 - kt;
-      if (steps < left) {
-        kt += steps;
-        t += steps;
-        return true;
-      }
-      steps -= left;
-      u += gridDim.x;
-      if (!load(p)) return false;
-    }
-    return true;
-  }
-};
-
-// Number of 32-entry groups of tile [a0, a1); 0 when malformed.
-__device__ __forceinline__ uint32_t tile_groups(const Params& p, uint32_t a0, uint32_t a1) {
-  return (a0 <= a1 && a1 <= p.n_entries && ((a1 - a0) & 31u) == 0) ? (a1 - a0) >> 5 : 0u;
-}
-
 // Byte offset of tile element `loc` (= x*64 + y) in the K-major SWIZZLE_NONE
-// canonical layout: (x/8)*1024 + (y/8)*128 + (x%8)*16 + (y%8)*2. Bits >= 13 of
-// loc are ignored, so the address is always inside the 16 KB tile.
-__device__ __forceinline__ uint32_t a_offset(uint32_t loc) {
-  return ((loc << 1) & 0x3C0Eu)  // (y%8)*2 from loc[2:0], (x/8)*1024 from loc[12:9]
-         | ((loc >> 2) & 0x70u)  // (x%8)*16 from loc[8:6]
-         | ((loc << 4) & 0x380u);  // (y/8)*128 from loc[5:3]
+// canonical layout: (x/8)*1024 + (y/8)*128 + (x%8)*16 + (y%8)*2, OR-ed into the
+// 16 KB-aligned tile base. Bits >= 13 of loc are ignored, so the address is
+// always inside the tile.
+__device__ __forceinline__ uint32_t a_addr(uint32_t a_tile, uint32_t loc) {
+  return (((loc << 1) & 0x3C0Eu) | a_tile)  // (y%8)*2 from loc[2:0], (x/8)*1024 from loc[12:9]
+         | ((loc >> 2) & 0x70u)            // (x%8)*16 from loc[8:6]
+         | ((loc << 4) & 0x380u);          // (y/8)*128 from loc[5:3]
 }
 
-__device__ __forceinline__ uint32_t ld_acquire_smem(uint32_t addr) {
+__device__ __forceinline__ void st_shared_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
-__device__ __forceinline__ void red_release_smem_add(uint32_t addr, uint32_t v) {
-  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+__device__ __forceinline__ void st_release_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
-__device__ __forceinline__ void st_shared_u32(uint32_t addr, uint32_t v) {
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+// Keeps a value in a register (stops ptxas from rematerialising smem bases
+// from %cluster_ctaid every time they are used).
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+  asm volatile("" : "+r"(v));
+  return v;
 }
-// Spin on an smem counter until it reaches `target` (watchdog as in mbar_wait).
-__device__ __forceinline__ void wait_counter(uint32_t addr, uint32_t target) {
-  if (static_cast<int32_t>(ld_acquire_smem(addr) - target) >= 0) return;
-  const long long t0 = clock64();
-  while (static_cast<int32_t>(ld_acquire_smem(addr) - target) < 0) {
-    if (clock64() - t0 > 40000000000LL) __trap();
+
+// Fall-through switches over a warp's group count: one indirect branch per
+// tile instead of a compare per group. Register arrays are indexed by constants.
+#define TCSL_DOWN16(X) \
+  X(15) X(14) X(13) X(12) X(11) X(10) X(9) X(8) X(7) X(6) X(5) X(4) X(3) X(2) X(1) X(0)
+#define TCSL_DOWN20(X) X(19) X(18) X(17) X(16) TCSL_DOWN16(X)
+
+__device__ __forceinline__ void load_groups(uint32_t (&E)[kGMax], uint32_t rbase, uint32_t cnt) {
+  switch (cnt) {
+#define TCSL_LD(J) \
+  case J + 1:      \
+    E[J] = lds32(rbase + (J) * 128u); [[fallthrough]];
+    default:
+      TCSL_DOWN20(TCSL_LD)
+    case 0:
+      break;
+#undef TCSL_LD
   }
 }
 
-// One decode warp's share of a team-tile: E holds its first kChunkG groups
-// (loaded earlier); meanwhile F is filled with its share of the team's next tile.
-template <int NA>
-__device__ __forceinline__ void decode_tile(const Params& p, uint32_t (&E)[kChunkG], uint32_t (&F)[kChunkG],
-                                            uint32_t a_tile, uint32_t a0, uint32_t g0, uint32_t g1,
-                                            uint32_t n0, uint32_t ng0, uint32_t ng1, int lane,
-                                            uint32_t& err_or) {
-  // Straight-line code in blocks of 8 groups: loads are unconditional (clamped to
-  // the last valid group), stores predicated in PTX — no per-group branches.
-  // Next team-tile's share first, so its L2 latency overlaps this tile's scatter.
-  const uint32_t ncnt = ng1 - ng0;
-  if (ncnt) {
-    const uint32_t* nsrc = p.ent + n0 + 32 * ng0 + lane;
-    const uint32_t last = ncnt - 1;
-#pragma unroll
-    for (int jb = 0; jb < kChunkG; jb += 8) {
-      if (static_cast<uint32_t>(jb) >= ncnt) break;
-#pragma unroll
-      for (int j = jb; j < jb + 8; ++j)
-        if (!DBG(32)) F[j] = ldg_stream(nsrc + 32 * min(static_cast<uint32_t>(j), last));
-    }
-  }
-  const uint32_t cnt = g1 - g0;
-#pragma unroll
-  for (int jb = 0; jb < kChunkG; jb += 8) {
-    if (static_cast<uint32_t>(jb) >= cnt) break;
-#pragma unroll
-    for (int j = jb; j < jb + 8; ++j) {
-      // slots past cnt hold duplicates of valid entries (or zeros): harmless for err_or
-      err_or |= E[j];
-      sts16_if(a_tile + a_offset(E[j]), E[j] >> 16, static_cast<uint32_t>(j) < cnt && !DBG(2));
-    }
-  }
-  // rare: more than kChunkG groups for this warp (density above ~25 %)
-  for (uint32_t g = g0 + kChunkG; g < g1; ++g) {
-    const uint32_t e = ldg_stream(p.ent + a0 + 32 * g + lane);
-    err_or |= e;
-    sts16(a_tile + a_offset(e), e >> 16);
+__device__ __forceinline__ void clear_groups(const uint32_t (&Z)[kGMax], uint32_t cnt) {
+  switch (cnt) {
+#define TCSL_CLR(J) \
+  case J + 1:       \
+    sts16(Z[J], 0u); [[fallthrough]];
+    default:
+      TCSL_DOWN20(TCSL_CLR)
+    case 0:
+      break;
+#undef TCSL_CLR
   }
 }
 
-template <int NPAD>
-__global__ void __launch_bounds__(kThreads, 1)
+__device__ __forceinline__ void scatter_groups(const uint32_t (&E)[kGMax], uint32_t (&Z)[kGMax], uint32_t cnt,
+                                               uint32_t a_tile) {
+  switch (cnt) {
+#define TCSL_SCAT(J)                                 \
+  case J + 1: {                                      \
+    const uint32_t a = a_addr(a_tile, E[J]);         \
+    sts16(a, E[J] >> 16);                            \
+    Z[J] = a;                                        \
+  }                                                  \
+    [[fallthrough]];
+    default:
+      TCSL_DOWN20(TCSL_SCAT)
+    case 0:
+      break;
+#undef TCSL_SCAT
+  }
+}
+
+struct Smem {
+  uint32_t a, ring, x;
+  uint32_t cfull, cempty, afull, aempty, xfull, xempty, dfull, dempty;
+  uint32_t meta, tab_s, tab_g0, tab_g1, ovf, tiles_ready, done, tab_ready, tmem_slot;
+};
+
+// Count a warp's consumed stream bytes [lo, hi) on the chunks' "consumed"
+// barriers (the stream warp refills a chunk once all of its bytes are consumed).
+__device__ __forceinline__ void release_ring(const Smem& s, uint32_t lo, uint32_t hi) {
+  for (uint32_t k = lo / kChunk; k <= (hi - 1) / kChunk; ++k) {
+    const uint32_t c0 = max(lo, k * kChunk), c1 = min(hi, (k + 1) * kChunk);
+    mbar_complete_tx(s.cempty + 8 * (k % kNR), c1 - c0);
+  }
+}
+
+// One decode warp's part of tile gt (see the file comment). Z / nz describe
+// what this warp last wrote into the tile's buffer.
+__device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint32_t gt, int team, int tw, int lane,
+                                            uint32_t afull_leader, uint32_t (&E)[kGMax], uint32_t (&Z)[kGMax],
+                                            uint32_t& nz, uint32_t& err_or) {
+  // per-tile metadata from the stream producer (normally published long ago)
+  HB(1, gt);
+  if (tw == 0 && lane == 0) TRACE(13, gt);
+  if (ld_acquire_u32(s.tiles_ready) <= gt) {
+    const long long t0 = clock64();
+    while (ld_acquire_u32(s.tiles_ready) <= gt) {
+      __nanosleep(32);
+      if (clock64() - t0 > 40000000000LL) __trap();
+    }
+  }
+  const uint2 meta = lds64(s.meta + 8 * (gt % kMeta));  // (stream offset, groups)
+  const uint32_t g0w = (meta.y * tw) >> 2, g1w = (meta.y * (tw + 1)) >> 2;
+  const uint32_t cnt = g1w - g0w;
+  const uint32_t ncnt = min(cnt, static_cast<uint32_t>(kGMax));
+  const uint32_t lo = meta.x + g0w * 128u, hi = meta.x + g1w * 128u;  // this warp's stream bytes
+  HB(2, gt);
+  if (cnt) {
+    for (uint32_t k = lo / kChunk; k <= (hi - 1) / kChunk; ++k)
+      mbar_wait_backoff(s.cfull + 8 * (k % kNB), (k / kNB) & 1, 64);
+    if (DBG(4)) {
+    } else if ((lo & (kRing - 1)) + cnt * 128u <= kRing) {
+      load_groups(E, s.ring + (lo & (kRing - 1)) + 4u * lane, ncnt);
+    } else {  // this warp's span wraps around the ring end
+#pragma unroll
+      for (int j = 0; j < kGMax; ++j)
+        if (static_cast<uint32_t>(j) < ncnt) E[j] = lds32(s.ring + ((lo + j * 128u) & (kRing - 1)) + 4u * lane);
+    }
+    // locations must stay inside the 128x64 tile; slots past ncnt hold this
+    // warp's earlier (already checked) entries
+#pragma unroll
+    for (int j = 0; j < kGMax; ++j) err_or |= E[j];
+    // the entries are in registers now (err_or consumed them): hand the ring
+    // bytes back at once so the stream refills while this tile is scattered
+    __syncwarp();
+    if (cnt <= static_cast<uint32_t>(kGMax) && lane == 0) release_ring(s, lo, hi);
+  }
+  if (tw == 0 && lane == 0) TRACE(14, gt);
+  const uint32_t b = gt % kNA;
+  const uint32_t a_tile = s.a + b * kABytes;
+  HB(3, gt);
+  if (gt >= static_cast<uint32_t>(kNA)) mbar_wait_backoff(s.aempty + 8 * b, ((gt / kNA) - 1) & 1, 64);
+  if (tw == 0 && lane == 0) TRACE(0, gt);
+  HB(4, gt);
+  // s.ovf[b] = the last tile in buffer b for which some warp of the team wrote
+  // more groups than it remembers: then the whole team clears by quarters.
+  if (gt >= static_cast<uint32_t>(kNA) && lds32(s.ovf + 4 * b) == gt - kNA) {
+    const uint32_t q0 = a_tile + tw * (kABytes / kTeamWarps);
+#pragma unroll
+    for (int r = 0; r < static_cast<int>(kABytes / kTeamWarps / 512); ++r) sts128_zero(q0 + 512 * r + 16 * lane);
+  } else if (!DBG(1)) {
+    clear_groups(Z, nz);
+  }
+  HB(5, gt);
+  named_bar_sync(1 + team, kTeamWarps * 32);
+  HB(6, gt);
+  if (tw == 0 && lane == 0) {
+    TRACE(1, gt);
+    asm volatile("red.relaxed.cta.shared::cta.add.u32 [%0], 1;" ::"r"(s.done) : "memory");  // meta slot read
+  }
+  if (!DBG(1)) scatter_groups(E, Z, ncnt, a_tile);
+  nz = DBG(1) ? 0 : ncnt;
+  if (cnt > static_cast<uint32_t>(kGMax)) {  // dense tiles (> ~25 % nonzeros)
+    for (uint32_t g = kGMax; g < cnt; ++g) {
+      const uint32_t e = lds32(s.ring + ((lo + g * 128u) & (kRing - 1)) + 4u * lane);
+      err_or |= e;
+      sts16(a_addr(a_tile, e), e >> 16);
+    }
+    if (lane == 0) st_shared_u32(s.ovf + 4 * b, gt);
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    // signal the MMA (an overflowed warp hands its ring bytes back only now)
+    if (cnt > static_cast<uint32_t>(kGMax)) release_ring(s, lo, hi);
+    mbar_arrive_cluster(afull_leader + 8 * b);
+  }
+  if (tw == 0 && lane == 0) TRACE(2, gt);
+  HB(7, gt);
+}
+
+template <int NH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     spmm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
-  using C = Cfg<NPAD>;
-  constexpr int NA = C::kNA;
+  using C = Cfg<NH>;
   constexpr int NX = C::kNX;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t s_a = (raw + 1023u) & ~1023u;
-  const uint32_t s_x = s_a + C::kOffX;
-  const uint32_t s_bar = s_a + C::kOffBar;
-  const uint32_t b_aempty = s_bar;  // [NA/2] MMAs of both tiles of a buffer pair complete
-  const uint32_t b_xfull = s_bar + 8 * (NA / 2), b_xempty = b_xfull + 8 * NX;
-  const uint32_t b_dfull = b_xempty + 8 * NX, b_dempty = b_dfull + 16;
-  const uint32_t s_flags = s_a + C::kOffFlags;  // [NA] decode-warp completions per buffer
-  const uint32_t s_tmem_slot = s_flags + 4 * NA;
-  const uint32_t s_progress = s_tmem_slot + 4;  // k-tiles the MMA has consumed (prefetch pacing)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (s_tmem_slot - raw));
-  volatile uint32_t* progress = reinterpret_cast<volatile uint32_t*>(smem_raw + (s_progress - raw));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t base = smem_u32(smem_raw);
+  Smem s;
+  s.ring = opaque(base + C::kOffRing);
+  s.x = opaque(base + C::kOffX);
+  s.a = opaque(((base + C::kOffA) + 16383u) & ~16383u);  // == base + kOffA when base % 16 KB == 1 KB
+  const uint32_t sm = base + C::kOffSmall;
+  s.cfull = opaque(sm);              // [kNB] ring chunk landed (bulk-copy bytes)
+  s.cempty = s.cfull + 8 * kNB;      // [kNR] ring chunk consumed (decoders' complete_tx bytes)
+  s.afull = s.cempty + 8 * kNR;      // [kNA] even CTA: 8 arrivals (4 decode warps x 2 CTAs)
+  s.aempty = s.afull + 8 * kNA;      // [kNA] both CTAs: MMA commit
+  s.xfull = s.aempty + 8 * kNA;      // [NX] even CTA: 2 arrivals + both halves' bytes
+  s.xempty = s.xfull + 8 * NX;       // [NX] both CTAs: MMA commit
+  s.dfull = s.xempty + 8 * NX;       // [2] both CTAs: MMA commit
+  s.dempty = s.dfull + 16;           // [2] even CTA: 8 arrivals (4 epilogue warps x 2 CTAs)
+  s.meta = s.dempty + 16;            // [kMeta] x (stream offset, groups)
+  s.tab_s = s.meta + 8 * kMeta;      // [kMaxUnits] unit table: stream offset of the unit
+  s.tab_g0 = s.tab_s + 4 * kMaxUnits;  // offsets[first tile]
+  s.tab_g1 = s.tab_g0 + 4 * kMaxUnits;  // offsets[last tile + 1] (== g0 for an invalid unit)
+  s.ovf = s.tab_g1 + 4 * kMaxUnits;  // [kNA]
+  s.tiles_ready = s.ovf + 4 * kNA;   // tiles with published metadata
+  s.done = s.tiles_ready + 4;        // tiles whose metadata the decoders have read
+  s.tab_ready = s.done + 4;          // unit table written (stream warp -> polling warp)
+  s.tmem_slot = s.tab_ready + 4;
+  static_assert(8 * (kNB + kNR + 2 * kNA + 2 * NX + 4 + kMeta) + 12 * kMaxUnits + 4 * kNA + 16 <= kSmallBytes,
+                "small smem region");
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (s.tmem_slot - base));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cid = static_cast<int>(cluster_id_x());
+  const int ncl = static_cast<int>(num_clusters_x());
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NA / 2; ++i) mbar_init(b_aempty + 8 * i, 1);
-    for (int i = 0; i < NA; ++i) st_shared_u32(s_flags + 4 * i, 0);
+    if (s.a + kNA * kABytes > base + C::kSmem) __trap();  // dynamic smem not placed as assumed
+    for (int i = 0; i < kNB; ++i) mbar_init(s.cfull + 8 * i, 1);
+    for (int i = 0; i < kNR; ++i) mbar_init(s.cempty + 8 * i, 1);
+    for (int i = 0; i < kNA; ++i) {
+      mbar_init(s.afull + 8 * i, 2 * kTeamWarps);
+      mbar_init(s.aempty + 8 * i, 1);
+      st_shared_u32(s.ovf + 4 * i, 0xFFFFFFFFu);
+    }
     for (int i = 0; i < NX; ++i) {
-      mbar_init(b_xfull + 8 * i, 1);
-      mbar_init(b_xempty + 8 * i, 1);
+      mbar_init(s.xfull + 8 * i, 2);
+      mbar_init(s.xempty + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(b_dfull + 8 * i, 1);
-      mbar_init(b_dempty + 8 * i, 4);
+      mbar_init(s.dfull + 8 * i, 1);
+      mbar_init(s.dempty + 8 * i, 8);
     }
-    *progress = 0;
+    st_shared_u32(s.tiles_ready, 0u);
+    st_shared_u32(s.done, 0u);
+    st_shared_u32(s.tab_ready, 0u);
     fence_barrier_init();
   }
-  if (warp == kWarpX && lane == 0) prefetch_tmap(&tmap_x);
-  if (warp == kWarpMma) tmem_alloc_dyn(s_tmem_slot, C::kTmemCols);
-  for (uint32_t i = threadIdx.x; i < NA * kABytes / 16; i += kThreads) sts128_zero(s_a + 16 * i);
+  if (warp == kWarpPoll && lane == 0) prefetch_tmap(&tmap_x);
+  if (warp == kWarpMma) tmem_alloc_pair(s.tmem_slot, C::kTmemCols);
+  for (uint32_t i = threadIdx.x; i < kNA * kABytes / 16; i += kThreads) sts128_zero(s.a + 16 * i);
+  HB(60, 0);
   fence_proxy_async_smem();
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrival
   tc_fence_after();
+  HB(61, 0);
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == kWarpX) {
-    // ---------------------------------------------------------------- X producer
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_last();
-      uint32_t gs = 0;  // global X stage counter
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const Unit un = unit_of(p, u);
-        for (int kt = un.kt0; kt < un.kt1; kt += C::kTX, ++gs) {
-          const uint32_t slot = gs % NX;
-          const uint32_t use = gs / NX;
-          if (use > 0) mbar_wait_sleep(b_xempty + 8 * slot, (use - 1) & 1);
-          mbar_arrive_expect_tx(b_xfull + 8 * slot, C::kXStage);
-#pragma unroll
-          for (int bx = 0; bx < C::kBoxes; ++bx)
-            tma_load_2d(s_x + slot * C::kXStage + bx * C::kBoxBytes, &tmap_x, p.col0 + bx * C::kBoxW, kt * kKTB,
-                        b_xfull + 8 * slot, pol);
-        }
-      }
-    }
-  } else if (warp == kWarpMma) {
-    // ---------------------------------------------------------------- MMA issuer
-    // The whole warp walks the schedule (warp-uniform values stay in uniform
-    // registers); one elected lane issues. Descriptors are base + byte offset/16.
-    const uint64_t a_desc0 = smem_desc(s_a, 128, 1024, 0);
-    const uint64_t b_desc0 = smem_desc(s_x, C::kLBO, C::kSBO, C::kLayout);
+  if (warp < kWarpEpi) {
+    // ---------------------------------------------------------------- decode teams
+    const int team = warp / kTeamWarps;
+    const int tw = warp % kTeamWarps;
     uint32_t total = 0;  // k-tiles of this CTA
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    for (int u = cid; u < p.units; u += ncl) {
       const Unit un = unit_of(p, u);
       total += un.kt1 - un.kt0;
     }
-    uint32_t gt = 0, ui = 0, gs = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
-      const Unit un = unit_of(p, u);
-      const uint32_t acc = ui & 1;
-      if (ui >= 2) mbar_wait_sleep(b_dempty + 8 * acc, ((ui >> 1) - 1) & 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem + acc * NPAD;
-      for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
-        const int in_stage = (kt - un.kt0) % C::kTX;
-        const uint32_t xs = gs % NX;
-        if (in_stage == 0) mbar_wait(b_xfull + 8 * xs, (gs / NX) & 1);
-        const uint32_t b = gt % NA;
-        if ((gt & 1u) == 0) {
-          // both tiles of the pair decoded? (one sync point per two k-tiles)
-          if (lane == 0) TRACE(5, gt);
-          wait_counter(s_flags + 4 * b, kTeamWarps * (gt / NA + 1));
-          if (gt + 1 < total) wait_counter(s_flags + 4 * (b + 1), kTeamWarps * ((gt + 1) / NA + 1));
-          if (lane == 0) TRACE(6, gt);
-          tc_fence_after();
-        }
-        const uint64_t ad = a_desc0 + ((b * kABytes) >> 4);
-        const uint64_t bd = b_desc0 + ((xs * C::kXStage + in_stage * C::kTileStep) >> 4);
-        if (elect_one()) {
+    const uint32_t afull_leader = mapa_shared(s.afull, 0);
+    uint32_t E[kGMax], Z[kGMax];
 #pragma unroll
-          for (int s = 0; s < kKTB / 16; ++s)
-            mma_f16_ss(d_tmem, ad + (s * 256 >> 4), bd + (s * C::kKStep >> 4), C::kIdesc,
-                       (kt > un.kt0 || s > 0) ? 1u : 0u);
-          if ((gt & 1u) || gt + 1 == total) mma_commit(b_aempty + 8 * (b >> 1));
-          if (in_stage == C::kTX - 1 || kt + 1 == un.kt1) mma_commit(b_xempty + 8 * xs);
-          if ((gt & 3u) == 3u) *progress = gt + 1;
-        }
-        __syncwarp();
-        if (in_stage == C::kTX - 1 || kt + 1 == un.kt1) ++gs;
-        if (lane == 0 && (gt & 1u)) TRACE(7, gt - 1);
-      }
-      if (elect_one()) mma_commit(b_dfull + 8 * acc);
-      __syncwarp();
-    }
-  } else if (warp == kWarpPf) {
-    // ---------------------------------------------------------------- L2 prefetcher
-    // Keeps the entry spans of the next kPrefetchAhead k-tiles on their way to
-    // L2 so the decode warps' loads hit L2 instead of waiting on HBM.
-    // A unit's tiles are contiguous in the entry array, so the warp prefetches
-    // chunks of kPfChunk tiles; each lane loads the bounds of one chunk (32
-    // chunks per offset round trip) and the chunks are issued in order, paced.
-    uint32_t base = 0;  // schedule index of the unit's first k-tile
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const Unit un = unit_of(p, u);
-      const uint32_t t0 = static_cast<uint32_t>(un.rb) * p.tiles_k + un.kt0;
-      const uint32_t nt = un.kt1 - un.kt0;
-      for (uint32_t c = 0; c < nt; c += 32 * kPfChunk) {
-        const uint32_t my0 = min(c + lane * kPfChunk, nt), my1 = min(my0 + kPfChunk, nt);
-        uint32_t lo = 0, hi = 0;
-        if (my1 > my0) {
-          lo = __ldg(p.off + t0 + my0);
-          hi = __ldg(p.off + t0 + my1);
-        }
-        const bool ok = hi > lo && hi <= p.n_entries && (lo & 3u) == 0;
-        for (int i = 0; i < 32; ++i) {
-          const uint32_t first = c + i * kPfChunk;
-          if (first >= nt) break;
-          if (lane == 0)
-            while (base + first >= *progress + kPrefetchAhead) __nanosleep(64);
-          __syncwarp();
-          if (lane == i && ok) bulk_prefetch_l2(p.ent + lo, ((hi - lo) * 4u) & ~15u);
-        }
-      }
-      base += nt;
-    }
-  } else if (warp >= kWarpEpi && warp < kWarpEpi + 4) {
+    for (int j = 0; j < kGMax; ++j) E[j] = 0u;  // slots past a tile's count keep older, checked entries
+    uint32_t nz = 0;
+    uint32_t err_or = 0;
+    for (uint32_t gt = team; gt < total; gt += kTeams)
+      decode_tile(p, s, gt, team, tw, lane, afull_leader, E, Z, nz, err_or);
+    // locations >= 8192 leave the 128x64 tile (the scatter masked them into range)
+    if (__any_sync(0xffffffffu, (err_or & 0xE000u) != 0) && lane == 0)
+      raise_dev(p.err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
+  } else if (warp < kWarpEpi + 4) {
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lanes 32q..32q+31
+    const uint32_t dempty_leader = mapa_shared(s.dempty, 0);
     uint32_t ui = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
+    for (int u = cid; u < p.units; u += ncl, ++ui) {
       const Unit un = unit_of(p, u);
       const uint32_t acc = ui & 1;
-      mbar_wait_sleep(b_dfull + 8 * acc, (ui >> 1) & 1);
+      HB(10, ui);
+      // woken by the polling warp once dfull[acc] has completed (a hardware
+      // barrier: no issue slots burnt while the unit is computed)
+      named_bar_sync(kBarEpi + acc, 5 * 32);
+      HB(11, ui);
       tc_fence_after();
-      const long long row = static_cast<long long>(un.rb) * kMTB + q * 32 + lane;
-      float* dst = p.out + (p.split > 1 ? static_cast<long long>(un.s) * p.m * p.ldo : 0ll) + row * p.ldo + p.col0;
-      const bool row_ok = row < p.m;
-      const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * NPAD;
-      const int ncol = min(NPAD, p.n - p.col0);
-      if constexpr (NPAD == 8) {
-        uint32_t r[8];
-        tmem_ld8(t_base, r);
-        tmem_ld_wait();
-        if (row_ok) {
-          if (ncol == 8 && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
-            reinterpret_cast<float4*>(dst)[0] =
-                make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3]));
-            reinterpret_cast<float4*>(dst)[1] =
-                make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7]));
-          } else {
+      const int rb = 2 * un.rp + static_cast<int>(rank);
+      const long long row = static_cast<long long>(rb) * kMTB + q * 32 + lane;
+      if (rb < p.tiles_m) {
+        float* dst =
+            p.out + (p.split > 1 ? static_cast<long long>(un.s) * p.m * p.ldo : 0ll) + row * p.ldo + p.col0;
+        const bool row_ok = row < p.m;
+        const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * C::kN;
+        const int ncol = min(C::kN, p.n - p.col0);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (j < ncol) dst[j] = __uint_as_float(r[j]);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int c0 = 0; c0 < NPAD; c0 += 16) {
+        for (int c0 = 0; c0 < C::kN; c0 += 16) {
           uint32_t r[16];
           tmem_ld16(t_base + c0, r);
           tmem_ld_wait();
@@ -436,106 +475,239 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(b_dempty + 8 * acc);
+      if (lane == 0) mbar_arrive_cluster(dempty_leader + 8 * acc);
     }
-  } else if (warp >= kWarpDec && warp < kWarpDec + kTeams * kTeamWarps) {
-    // ---------------------------------------------------------------- decode teams
-    // Team t owns the k-tiles gt = t, t + kTeams, ...; each of its 4 warps owns a
-    // contiguous quarter of the tile's groups. Two register sets alternate
-    // between team-tiles (no copies): while one tile is scattered, the next
-    // team-tile's entries are in flight; offsets run two team-tiles ahead.
-    const int dw = warp - kWarpDec;
-    const int team = dw / kTeamWarps;
-    const int tw = dw % kTeamWarps;
-    TileWalk w;
-    bool more = w.start(p) && w.advance(p, team);
-    uint32_t gt = team;
-    uint32_t err_or = 0;
-    bool bad_off = false;
-    uint32_t a0 = 0, a1 = 0, n0 = 0, n1 = 0;
-    uint32_t E0[kChunkG], E1[kChunkG];
-#pragma unroll
-    for (int j = 0; j < kChunkG; ++j) E0[j] = E1[j] = 0u;  // unused slots must not look like bad locations
-    bool has_n = false;
-    if (more) {
-      a0 = __ldg(p.off + w.t);
-      a1 = __ldg(p.off + w.t + 1);
-      const uint32_t ng = tile_groups(p, a0, a1);
-      const uint32_t g0 = ng * tw / kTeamWarps, g1 = ng * (tw + 1) / kTeamWarps;
-#pragma unroll
-      for (int j = 0; j < kChunkG; ++j)
-        if (g0 + j < g1) E0[j] = ldg_stream(p.ent + a0 + 32 * (g0 + j) + lane);
-      has_n = w.advance(p, kTeams);
-      if (has_n) {
-        n0 = __ldg(p.off + w.t);
-        n1 = __ldg(p.off + w.t + 1);
+  } else if (warp == kWarpStream) {
+    // ---------------------------------------------------------------- entry stream
+    // The CTA's entry stream is the concatenation of its units' entry ranges
+    // [offsets[first tile], offsets[last tile + 1]) (contiguous per unit: tiles are
+    // row-major over the tile grid, tcsl_format.cpp:56-57). Stream byte S lives at
+    // ring offset S % kRing and is fetched in kChunk-byte bulk copies (split at
+    // unit boundaries); chunk k lands on cfull[k % kNB], decoders count consumed
+    // bytes on cempty[k % kNR] (complete_tx). A bulk-copy issue blocks for
+    // hundreds of cycles under load, so this warp does nothing else.
+    // 1. Validate every unit (monotone offsets, whole 32-entry groups, in range)
+    //    into the unit table; an invalid unit streams no bytes and its tiles
+    //    decode as empty (the error is reported).
+    uint32_t total = 0, nunits = 0;
+    for (int u = cid; u < p.units; u += ncl, ++nunits) {
+      const Unit un = unit_of(p, u);
+      const int rb = 2 * un.rp + static_cast<int>(rank);
+      const uint32_t nt = un.kt1 - un.kt0;
+      uint32_t g0 = 0, g1 = 0;
+      if (rb < p.tiles_m) {
+        const uint32_t t0 = static_cast<uint32_t>(rb) * p.tiles_k + un.kt0;
+        g0 = __ldg(p.off + t0);
+        g1 = __ldg(p.off + t0 + nt);
+        bool bad = g0 > g1 || g1 > p.n_entries || (g0 & 31u) != 0;
+#pragma unroll 4
+        for (uint32_t i = lane; i < nt; i += 32) {
+          const uint32_t a = __ldg(p.off + t0 + i), b = __ldg(p.off + t0 + i + 1);
+          bad |= b < a || ((b - a) & 31u) != 0;
+        }
+        if (__any_sync(0xffffffffu, bad)) {
+          if (lane == 0) raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
+          g1 = g0;
+        }
       }
-    }
-    int parity = 0;  // which register set holds the current tile
-    while (more) {
-      const uint32_t ng = tile_groups(p, a0, a1);
-      if (a1 != a0 + 32 * ng) bad_off = true;
-      const uint32_t g0 = ng * tw / kTeamWarps, g1 = ng * (tw + 1) / kTeamWarps;
-      // offsets of the team's tile after next
-      const bool has_nn = has_n && w.advance(p, kTeams);
-      uint32_t nn0 = 0, nn1 = 0;
-      if (has_nn) {
-        nn0 = __ldg(p.off + w.t);
-        nn1 = __ldg(p.off + w.t + 1);
-      }
-      const uint32_t nng = has_n ? tile_groups(p, n0, n1) : 0u;
-      const uint32_t ng0 = nng * tw / kTeamWarps, ng1 = nng * (tw + 1) / kTeamWarps;
-
-      const uint32_t b = gt % NA;
-      const uint32_t use = gt / NA;
-      const uint32_t a_tile = s_a + b * kABytes;
-      if (tw == 0 && lane == 0) TRACE(0, gt);
-      if (use > 0) {
-        // sleep in hardware: spinning try_waits from 12 warps starve the tcgen05 issue path
-        mbar_wait_sleep(b_aempty + 8 * (b >> 1), (use - 1) & 1);
-        const uint32_t q0 = a_tile + tw * (kABytes / kTeamWarps);
-#pragma unroll
-        for (int r = 0; r < static_cast<int>(kABytes / kTeamWarps / 512); ++r)
-          if (!DBG(4)) sts128_zero(q0 + 512 * r + 16 * lane);
-      }
-      if (tw == 0 && lane == 0) TRACE(1, gt);
-      named_bar_sync(1 + team, kTeamWarps * 32);
-      if (tw == 0 && lane == 0) TRACE(2, gt);
-      if (DBG(1024)) {
-      } else if (parity == 0)
-        decode_tile<NA>(p, E0, E1, a_tile, a0, g0, g1, n0, ng0, ng1, lane, err_or);
-      else
-        decode_tile<NA>(p, E1, E0, a_tile, a0, g0, g1, n0, ng0, ng1, lane, err_or);
-      if (tw == 0 && lane == 0) TRACE(3, gt);
-      if (!DBG(64)) fence_proxy_async_smem();
-      __syncwarp();
       if (lane == 0) {
-        if (DBG(128))
-          asm volatile("red.relaxed.cta.shared::cta.add.u32 [%0], %1;" ::"r"(s_flags + 4 * b), "r"(1u) : "memory");
-        else
-          red_release_smem_add(s_flags + 4 * b, 1u);
+        st_shared_u32(s.tab_s + 4 * nunits, total);
+        st_shared_u32(s.tab_g0 + 4 * nunits, g0);
+        st_shared_u32(s.tab_g1 + 4 * nunits, g1);
       }
-      if (tw == 0 && lane == 0) TRACE(4, gt);
-      parity ^= 1;
-      more = has_n;
-      a0 = n0;
-      a1 = n1;
-      has_n = has_nn;
-      n0 = nn0;
-      n1 = nn1;
-      gt += kTeams;
+      total += (g1 - g0) * 4u;
     }
-    // locations >= 8192 leave the 128x64 tile (the scatter masked them into range)
-    if (__any_sync(0xffffffffu, (err_or & 0xE000u) != 0) && lane == 0)
-      raise_dev(p.err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
-    if (__any_sync(0xffffffffu, bad_off) && lane == 0) raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
+    __syncwarp();
+    if (lane == 0) {
+      st_release_u32(s.tab_ready, 1u);  // unit table complete (read by the polling warp)
+      // 2. Stream.
+      const uint64_t pol = policy_evict_first();
+      const uint32_t nchunks = (total + kChunk - 1) / kChunk;
+      uint32_t iu = 0, us = 0, ug0 = 0, ue = 0;  // unit holding the next byte (cached)
+      bool have_unit = false;
+      for (uint32_t k = 0; k < nchunks; ++k) {
+        const uint32_t c0 = k * kChunk, c1 = min(total, c0 + kChunk);
+        if (k >= static_cast<uint32_t>(kNR)) mbar_wait(s.cempty + 8 * (k % kNR), ((k / kNR) - 1) & 1);
+        mbar_arrive_expect_tx(s.cempty + 8 * (k % kNR), c1 - c0);
+        mbar_arrive_expect_tx(s.cfull + 8 * (k % kNB), c1 - c0);
+        for (uint32_t pos = c0; pos < c1;) {
+          if (!have_unit || pos >= ue) {
+            if (have_unit) ++iu;
+            us = lds32(s.tab_s + 4 * iu);
+            ug0 = lds32(s.tab_g0 + 4 * iu);
+            ue = us + (lds32(s.tab_g1 + 4 * iu) - ug0) * 4u;
+            have_unit = true;
+            continue;
+          }
+          const uint32_t pe = min(c1, ue);
+          bulk_g2s(s.ring + (pos & (kRing - 1)), p.ent + ug0 + (pos - us) / 4u, pe - pos, s.cfull + 8 * (k % kNB),
+                   pol);
+          TRACE(6, k);
+          pos = pe;
+        }
+      }
+    }
+  } else if (warp == kWarpPoll) {
+    // ---------------------------------------------------------------- polling warp
+    // Non-blocking checks only (mbarrier.test_wait): (a) per-tile metadata
+    // (stream offset, groups), 32 tiles per step, one lane per tile, offsets
+    // loaded one step ahead; (b) X stages (TMA, this CTA's half of the B
+    // columns); (c) epilogue wake-ups (named barrier per accumulator).
+    uint32_t nunits = 0, ntiles = 0, nstages = 0;
+    for (int u = cid; u < p.units; u += ncl, ++nunits) {
+      const Unit un = unit_of(p, u);
+      ntiles += un.kt1 - un.kt0;
+      nstages += (un.kt1 - un.kt0 + C::kTX - 1) / C::kTX;
+    }
+    const uint64_t pol_x = policy_evict_last();
+    const uint32_t xfull_leader = mapa_shared(s.xfull, 0);
+    uint32_t gt = 0, mu = 0, mkt = 0;  // (a) next tile to publish: unit ordinal, k-tile within the unit
+    int mu_id = cid;
+    uint32_t pend = 0, pa0 = 0, pa1 = 0;  //     prefetched batch: tile count, this lane's offsets
+    uint32_t gs = 0, xkt = 0;          // (b) next X stage; its first k-tile within the unit
+    int xu_id = cid;
+    uint32_t eu = 0;                   // (c) next unit whose accumulator the epilogue waits for
+    auto prefetch_batch = [&]() {
+      const Unit un = unit_of(p, mu_id);
+      const int rb = 2 * un.rp + static_cast<int>(rank);
+      pend = min(32u, static_cast<uint32_t>(un.kt1 - un.kt0) - mkt);
+      pa0 = pa1 = 0;
+      if (rb < p.tiles_m && lane < pend) {
+        const uint32_t t = static_cast<uint32_t>(rb) * p.tiles_k + un.kt0 + mkt + lane;
+        pa0 = __ldg(p.off + t);
+        pa1 = __ldg(p.off + t + 1);
+      }
+    };
+    if (ntiles) prefetch_batch();
+    bool tab = false;
+    long long idle_t0 = clock64();
+    while (gt < ntiles || gs < nstages || eu < nunits) {
+      bool progress = false;
+      if (lane == 0) {
+        // (b) X stages
+        while (gs < nstages && (gs < static_cast<uint32_t>(NX) || mbar_test_wait(s.xempty + 8 * (gs % NX), ((gs / NX) - 1) & 1))) {
+          const Unit un = unit_of(p, xu_id);
+          const uint32_t slot = gs % NX;
+          mbar_arrive_expect_tx_cluster(xfull_leader + 8 * slot, C::kXStage);
+#pragma unroll
+          for (int bx = 0; bx < C::kBoxes; ++bx)
+            tma_load_2d_pair(s.x + slot * C::kXStage + bx * C::kBoxBytes, &tmap_x,
+                             p.col0 + static_cast<int>(rank) * NH + bx * C::kBoxW,
+                             (un.kt0 + static_cast<int>(xkt)) * kKTB, xfull_leader + 8 * slot, pol_x);
+          TRACE(5, gs);
+          ++gs;
+          xkt += C::kTX;
+          if (xkt >= static_cast<uint32_t>(un.kt1 - un.kt0)) {
+            xkt = 0;
+            xu_id += ncl;
+          }
+          progress = true;
+        }
+      }
+      // lane 0 advanced gs / xkt / xu_id: broadcast (warp-uniform loop state)
+      progress = __shfl_sync(0xffffffffu, progress, 0);
+      gs = __shfl_sync(0xffffffffu, gs, 0);
+      xkt = __shfl_sync(0xffffffffu, xkt, 0);
+      xu_id = __shfl_sync(0xffffffffu, xu_id, 0);
+      // (c) epilogue wake-ups (the whole warp arrives on the named barrier)
+      while (eu < nunits && __shfl_sync(0xffffffffu, mbar_test_wait(s.dfull + 8 * (eu & 1), (eu >> 1) & 1) ? 1 : 0, 0)) {
+        asm volatile("bar.arrive %0, %1;" ::"r"(kBarEpi + (eu & 1)), "r"(5 * 32) : "memory");
+        ++eu;
+        progress = true;
+      }
+      // (a) publish the prefetched batch when the unit table is ready and the
+      //     metadata ring has room (one read, broadcast: uniform decisions)
+      if (!tab) tab = __shfl_sync(0xffffffffu, ld_acquire_u32(s.tab_ready), 0) != 0;
+      if (pend && tab) {
+        const uint32_t room = __shfl_sync(0xffffffffu, ld_acquire_u32(s.done), 0) + (kMeta - 16);
+        if (gt + pend <= room) {
+          if (lane < pend) {
+            const uint32_t g0 = lds32(s.tab_g0 + 4 * mu), g1 = lds32(s.tab_g1 + 4 * mu);
+            uint32_t so = lds32(s.tab_s + 4 * mu), ng = 0;
+            if (g1 > g0) {  // real rows of a valid, non-empty unit
+              so += (pa0 - g0) * 4u;
+              ng = (pa1 - pa0) >> 5;
+            }
+            st_shared_v2(s.meta + 8 * ((gt + lane) % kMeta), so, ng);
+          }
+          __threadfence_block();
+          __syncwarp();
+          gt += pend;
+          mkt += pend;
+          const Unit un = unit_of(p, mu_id);
+          if (mkt == static_cast<uint32_t>(un.kt1 - un.kt0)) {
+            mkt = 0;
+            ++mu;
+            mu_id += ncl;
+          }
+          pend = 0;
+          if (lane == 0) {
+            st_release_u32(s.tiles_ready, gt);
+            TRACE(10, gt / 32);
+          }
+          if (gt < ntiles) prefetch_batch();
+          progress = true;
+        }
+      }
+      if (progress) {
+        idle_t0 = clock64();
+      } else if (clock64() - idle_t0 > 40000000000LL) {
+        __trap();  // watchdog, as in mbar_wait
+      }
+    }
+  } else if (warp == kWarpMma && rank == 0) {
+    // ---------------------------------------------------------------- MMA issuer (even CTA)
+    // The whole warp walks the schedule; one elected lane issues.
+    const uint64_t a_desc0 = smem_desc(s.a, 128, 1024, 0);
+    const uint64_t b_desc0 = smem_desc(s.x, C::kLBO, C::kSBO, C::kLayout);
+    uint32_t gt = 0, ui = 0, gs = 0;
+    for (int u = cid; u < p.units; u += ncl, ++ui) {
+      const Unit un = unit_of(p, u);
+      const uint32_t acc = ui & 1;
+      if (ui >= 2) mbar_wait_cluster(s.dempty + 8 * acc, ((ui >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * C::kN;
+      for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
+        const int in_stage = (kt - un.kt0) % C::kTX;
+        const uint32_t xs = gs % NX;
+        HB(40, gt);
+        if (lane == 0) TRACE(8, gt);
+        if (in_stage == 0) mbar_wait_cluster(s.xfull + 8 * xs, (gs / NX) & 1);
+        const uint32_t b = gt % kNA;
+        if (lane == 0) TRACE(3, gt);
+        HB(41, gt);
+        mbar_wait_cluster(s.afull + 8 * b, (gt / kNA) & 1);
+        HB(42, gt);
+        if (lane == 0) TRACE(4, gt);
+        tc_fence_after();
+        const uint64_t ad = a_desc0 + ((b * kABytes) >> 4);
+        const uint64_t bd = b_desc0 + ((xs * C::kXStage + in_stage * C::kTileStep) >> 4);
+        const bool stage_done = in_stage == C::kTX - 1 || kt + 1 == un.kt1;
+        if (elect_one()) {
+#pragma unroll
+          for (int k4 = 0; k4 < kKTB / 16; ++k4)
+            if (!DBG(2))
+              mma_f16_ss_pair(d_tmem, ad + (k4 * 256 >> 4), bd + (k4 * C::kKStep >> 4), C::kIdesc,
+                              (kt > un.kt0 || k4 > 0) ? 1u : 0u);
+          mma_commit_pair(s.aempty + 8 * b, 3);
+          if (stage_done) mma_commit_pair(s.xempty + 8 * xs, 3);
+        }
+        __syncwarp();
+        if (stage_done) ++gs;
+      }
+      if (elect_one()) mma_commit_pair(s.dfull + 8 * acc, 3);
+      __syncwarp();
+    }
   }
 
+  __syncwarp();  // role branches may leave lanes behind; the cluster barrier is .aligned
+  HB(50, 0);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();
+  HB(51, 0);
   if (warp == kWarpMma) {
     tc_fence_after();
-    tmem_dealloc(tmem, C::kTmemCols);
+    tmem_dealloc_pair(tmem, C::kTmemCols);
   }
 }
 
@@ -551,20 +723,48 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-int pad_n(int n) {
-  if (n <= 8) return 8;
-  if (n <= 16) return 16;
-  if (n <= 32) return 32;
-  if (n <= 64) return 64;
-  if (n <= 128) return 128;
-  return 256;
+// Half-width (columns per CTA) for a slab of n <= 256 columns: MMA N = 2 * NH >= 16.
+int half_n(int n) {
+  if (n <= 16) return 8;
+  if (n <= 32) return 16;
+  if (n <= 64) return 32;
+  if (n <= 128) return 64;
+  return 128;
 }
 
-// Estimated runtime (us) of a split choice: max over persistent CTAs of their
+template <int NH>
+int max_clusters() {
+  static int cached = 0;
+  if (!cached) {
+    using C = Cfg<NH>;
+    cudaFuncSetAttribute(spmm_sm100_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(C::kSmem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * 74, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, spmm_sm100_kernel<NH>, &cfg) != cudaSuccess || nc <= 0) {
+      cudaGetLastError();
+      nc = num_sms() / 2;
+    }
+    cached = nc;
+  }
+  return cached;
+}
+
+// Estimated runtime (us) of a split choice: max over persistent pairs of their
 // units' tile work + per-unit overhead, plus the reduction pass.
-double split_cost(int tiles_m, int tiles_k, int split, int sms, double t_tile, double mn_bytes) {
-  const int units = tiles_m * split;
-  const int grid = std::min(units, sms);
+double split_cost(int tiles_mp, int tiles_k, int split, int clusters, double t_tile, double mn_bytes) {
+  const int units = tiles_mp * split;
+  const int grid = std::min(units, clusters);
   std::vector<double> load(grid, 0.0);
   for (int u = 0; u < units; ++u) {
     const int s = u % split;
@@ -578,18 +778,13 @@ double split_cost(int tiles_m, int tiles_k, int split, int sms, double t_tile, d
   return worst;
 }
 
-template <int NPAD>
-cudaError_t launch_npad(const Params& p, const CUtensorMap& tm, int grid, cudaStream_t s) {
-  using C = Cfg<NPAD>;
+template <int NH>
+cudaError_t launch_nh(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
+  using C = Cfg<NH>;
   static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(spmm_sm100_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(C::kSmem));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  spmm_sm100_kernel<NPAD><<<grid, kThreads, C::kSmem, s>>>(tm, p);
+  const int nc = std::min(clusters, max_clusters<NH>());
+  if ((p.units + nc - 1) / nc > kMaxUnits) return cudaErrorInvalidConfiguration;  // unit table size
+  spmm_sm100_kernel<NH><<<2 * nc, kThreads, C::kSmem, s>>>(tm, p);
   return cudaGetLastError();
 }
 
@@ -601,37 +796,46 @@ int num_sms() {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+      cudaGetLastError();
+      sms = 148;
+    }
   }
   return sms;
 }
 
 int auto_split(uint32_t m, uint32_t k, int n, double avg_entries_per_tile) {
   const int tiles_m = div_up_i(m, kMTB), tiles_k = div_up_i(k, kKTB);
-  const int sms = num_sms();
-  // per-SM streaming rate ~ 6.5 TB/s / 148; MMA floor ~0.1 us per tile
-  const double t_tile = std::max(avg_entries_per_tile * 4.0 / 44.0e3, 0.1);
+  const int tiles_mp = (tiles_m + 1) / 2;
+  const int clusters = num_sms() / 2;
+  // per-SM streaming rate ~ 6.5 TB/s / 148; MMA floor ~0.05 us per tile (CTA pair)
+  const double t_tile = std::max(avg_entries_per_tile * 4.0 / 44.0e3, 0.05);
   const double mn_bytes = static_cast<double>(m) * std::min(n, 256) * 4.0;
   int best = 1;
-  double best_cost = split_cost(tiles_m, tiles_k, 1, sms, t_tile, mn_bytes);
+  double best_cost = split_cost(tiles_mp, tiles_k, 1, clusters, t_tile, mn_bytes);
   for (int s = 2; s <= std::min(32, tiles_k); ++s) {
-    const double c = split_cost(tiles_m, tiles_k, s, sms, t_tile, mn_bytes);
+    const double c = split_cost(tiles_mp, tiles_k, s, clusters, t_tile, mn_bytes);
     if (c < best_cost * 0.97) {
       best = s;
       best_cost = c;
     }
   }
+  (void)n;
   return best;
 }
 
 int spmm_sm100_plan(uint32_t m, uint32_t k, int n, int split_k, SpmmPlan* plan) {
   const int tiles_m = div_up_i(m, kMTB), tiles_k = div_up_i(k, kKTB);
   plan->n = n;
-  plan->n_pad = pad_n(std::min(n, 256));
+  plan->n_pad = 2 * half_n(std::min(n, 256));
   plan->split = split_k > 0 ? std::min(split_k, tiles_k) : 1;
-  plan->units = tiles_m * plan->split;
-  plan->grid = std::min(plan->units, num_sms());
+  // each CTA pair keeps a table of at most kMaxUnits work units
+  const int tiles_mp = (tiles_m + 1) / 2;
+  const int cl = std::max(1, num_sms() / 2 - 4);
+  while (plan->split > 1 && (tiles_mp * plan->split + cl - 1) / cl > kMaxUnits) --plan->split;
+  plan->units = tiles_mp * plan->split;
+  plan->grid = std::min(plan->units, num_sms() / 2);  // CTA pairs
   plan->smem = 0;
   return 0;
 }
@@ -649,6 +853,7 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
   p.k = k;
   p.tiles_m = div_up_i(m, kMTB);
   p.tiles_k = div_up_i(k, kKTB);
+  p.tiles_mp = (p.tiles_m + 1) / 2;
   p.n = plan.n;
   p.split = plan.split;
   p.units = plan.units;
@@ -656,17 +861,13 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
   p.ldo = plan.n;
   p.err = err;
   p.trace = g_trace;
-#ifdef TCSL_TRACE
-  {
-    const int dbg = getenv("TCSL_DEBUG") ? atoi(getenv("TCSL_DEBUG")) : 0;
-    cudaMemcpyToSymbolAsync(c_debug, &dbg, sizeof dbg, 0, cudaMemcpyHostToDevice, s);
-  }
-#endif
+  static const int dbg_env = getenv("TCSL_DEBUG") ? atoi(getenv("TCSL_DEBUG")) : 0;
+  p.dbg = dbg_env;
   // Column slabs of <= 256 (one TMEM accumulator pair each).
   for (int col0 = 0; col0 < plan.n; col0 += 256) {
-    const int n_pad = pad_n(std::min(256, plan.n - col0));
-    const int box_w = std::min(n_pad, 64);
-    const int box_rows = 64 * (n_pad <= 32 ? 4 : (n_pad == 64 ? 2 : 1));  // Cfg<NPAD>::kTX k-tiles per stage
+    const int nh = half_n(std::min(256, plan.n - col0));
+    const int box_w = std::min(nh, 64);
+    const int box_rows = 64 * (nh <= 32 ? 4 : (nh == 64 ? 2 : 1));  // Cfg<NH>::kTX k-tiles per stage
     p.col0 = col0;
     const uint32_t row_bytes = box_w * 2;
     const CUtensorMapSwizzle swz =
@@ -683,13 +884,12 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     cudaError_t e;
-    switch (n_pad) {
-      case 8: e = launch_npad<8>(p, tm, plan.grid, s); break;
-      case 16: e = launch_npad<16>(p, tm, plan.grid, s); break;
-      case 32: e = launch_npad<32>(p, tm, plan.grid, s); break;
-      case 64: e = launch_npad<64>(p, tm, plan.grid, s); break;
-      case 128: e = launch_npad<128>(p, tm, plan.grid, s); break;
-      default: e = launch_npad<256>(p, tm, plan.grid, s); break;
+    switch (nh) {
+      case 8: e = launch_nh<8>(p, tm, plan.grid, s); break;
+      case 16: e = launch_nh<16>(p, tm, plan.grid, s); break;
+      case 32: e = launch_nh<32>(p, tm, plan.grid, s); break;
+      case 64: e = launch_nh<64>(p, tm, plan.grid, s); break;
+      default: e = launch_nh<128>(p, tm, plan.grid, s); break;
     }
     if (e != cudaSuccess) return e;
   }
@@ -700,4 +900,16 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
 
 #ifdef TCSL_TRACE
 extern "C" void tcsl_cuda_debug_set_trace(unsigned long long* d_trace) { tcslk::g_trace = d_trace; }
+#endif
+#if defined(TCSL_TRACE) && defined(TCSL_HEARTBEAT)
+// Allocates the mapped-host heartbeat array (148 CTAs x 32 warp slots) and returns its host address.
+extern "C" unsigned* tcsl_cuda_debug_heartbeat(void) {
+  unsigned* h = nullptr;
+  if (cudaHostAlloc(&h, 148 * 32 * 4, cudaHostAllocMapped) != cudaSuccess) return nullptr;
+  for (int i = 0; i < 148 * 32; ++i) h[i] = 0xFFFFFFFFu;
+  unsigned* d = nullptr;
+  cudaHostGetDevicePointer(&d, h, 0);
+  cudaMemcpyToSymbol(tcslk::g_hb, &d, sizeof d);
+  return h;
+}
 #endif

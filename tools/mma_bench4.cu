@@ -9,14 +9,7 @@
 
 using namespace tcslk;
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
+__device__ __forceinline__ uint32_t cluster_rank() { return cluster_ctarank(); }
 __device__ __forceinline__ void mma2_f16_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -30,7 +23,7 @@ __device__ __forceinline__ void commit2_mc(uint32_t bar, uint16_t mask) {
                : "memory");
 }
 
-template <int N, int PAIR>
+template <int N, int PAIR, int COMMIT_EVERY = 0>
 __global__ void __cluster_dims__(2, 1, 1) bench(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t base = (smem_u32(smem) + 1023u) & ~1023u;
@@ -41,6 +34,7 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int iters, unsigned long long* o
   for (int i = threadIdx.x; i < (4 * 16384 + 16384) / 16; i += blockDim.x) sts128_zero(base + 16 * i);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar + 8, 1);
     fence_barrier_init();
   }
   if (warp == 0) {
@@ -71,6 +65,12 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int iters, unsigned long long* o
         else
           mma_f16_ss(tmem, ad, bd, idesc, it > 0 ? 1u : 0u);
       }
+      if (COMMIT_EVERY && (it % COMMIT_EVERY) == COMMIT_EVERY - 1) {
+        if (PAIR)
+          commit2_mc(bar + 8, 3);
+        else
+          mma_commit(bar + 8);
+      }
     }
     if (PAIR)
       commit2_mc(bar, 3);
@@ -92,32 +92,33 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int iters, unsigned long long* o
   }
 }
 
-template <int N, int PAIR>
+template <int N, int PAIR, int COMMIT_EVERY = 0>
 void run() {
   unsigned long long* d;
   cudaMalloc(&d, 148 * 8);
   const int smem = 5 * 16384 + 2048;
-  cudaFuncSetAttribute(bench<N, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<N, PAIR, COMMIT_EVERY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 4096;
-  bench<N, PAIR><<<148, 128, smem>>>(iters, d);
-  bench<N, PAIR><<<148, 128, smem>>>(iters, d);
+  bench<N, PAIR, COMMIT_EVERY><<<148, 128, smem>>>(iters, d);
+  bench<N, PAIR, COMMIT_EVERY><<<148, 128, smem>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[148];
   cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
   double mx = 0;
   for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
-  printf("%s N=%3d: %6.1f cycles per instruction; %6.1f cycles per 128x64 tile per SM [%s]\n",
-         PAIR ? "cta_group::2 M=256" : "cta_group::1 M=128", N, mx / iters / 4, mx / iters / (PAIR ? 2 : 1),
+  printf("%s N=%3d commit every %d tiles: %6.1f cycles per instruction; %6.1f cycles per 128x64 tile per SM [%s]\n",
+         PAIR ? "cta_group::2 M=256" : "cta_group::1 M=128", N, COMMIT_EVERY, mx / iters / 4, mx / iters / (PAIR ? 2 : 1),
          cudaGetErrorString(e));
   cudaFree(d);
 }
 
 int main() {
-  run<16, 0>();
   run<16, 1>();
-  run<32, 1>();
-  run<64, 0>();
-  run<64, 1>();
-  run<128, 1>();
+  run<16, 1, 1>();
+  run<16, 1, 2>();
+  run<16, 1, 4>();
+  run<16, 0>();
+  run<16, 0, 1>();
+  run<64, 1, 1>();
   return 0;
 }

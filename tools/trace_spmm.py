@@ -42,7 +42,7 @@ torch.cuda.synchronize()
 L.tcsl_cuda_debug_set_trace(None)
 print(f"M={M} K={K} N={N} beta={beta} split={split or tc.auto_split(M, K, N)}: {s.elapsed_time(e) * 1e3:.1f} us")
 tr = trace.view(16, 4096).cpu().numpy().astype(np.int64)
-n = int((tr[5] > 0).sum())
+n = int((tr[4] > 0).sum())
 
 
 def st(name, v):
@@ -57,13 +57,34 @@ def diff(a, b):
     return (tr[b] - tr[a])[m][2:-2].astype(float)
 
 
-st("decode: wait aempty + zero (s1-s0)", diff(0, 1))
-st("decode: team barrier (s2-s1)", diff(1, 2))
-st("decode: scatter own groups (s3-s2)", diff(2, 3))
-st("decode: fence + flag (s4-s3)", diff(3, 4))
+st("decode: buffer ready -> team barrier passed (s1-s0)", diff(0, 1))
+st("decode: barrier -> tile done (s2-s1)", diff(1, 2))
 d0 = tr[0][:n][tr[0][:n] != 0]
 st("decode: team-tile period (team of tile 0)", np.diff(d0[::3]).astype(float)[1:-1])
-st("mma: wait decode flag (s6-s5)", diff(5, 6))
-st("mma: issue 4 MMAs + commits (s7-s6)", diff(6, 7))
-st("mma: tile period (s5[i+1]-s5[i])", np.diff(tr[5][:n]).astype(float)[2:-2])
-print(f"  tiles traced {n}, total cycles {tr[7][n - 1] - tr[5][0]}")
+st("mma: wait A full (s4-s3)", diff(3, 4))
+m3 = tr[3][:n].astype(float)
+st("mma: tile period (s3[i+1]-s3[i])", np.diff(m3)[2:-2])
+st("decode done -> mma sees it (s4 - s2)", diff(2, 4))
+print(f"  tiles traced {n}, total cycles {tr[4][n - 1] - tr[3][0]}")
+st("mma: wait X stage (s3 - s8)", diff(8, 3))
+base = tr[8][0]
+xs = tr[5][tr[5] != 0] - base
+ch = tr[6][tr[6] != 0] - base
+print("  X stage issue times (cycles from first MMA poll):", xs[:12].tolist())
+print("  MMA tile-start times:", (tr[8][:48:4] - base).tolist())
+print("  chunk issue times:", ch[:24].tolist())
+print("  decode tile-ready times (s0):", (tr[0][:24] - base).tolist())
+it = tr[9][tr[9] != 0] - base
+print("  poller: pass-1 start", tr[12][0] - base, "loop start", tr[11][0] - base, "iterations traced", it.size)
+print("  poller iteration times:", it[:40].tolist())
+print("  poller iteration period p50", float(np.median(np.diff(it))) if it.size > 2 else None)
+print("  meta publish times (per 32 tiles):", (tr[10][:8] - base).tolist())
+# per-tile critical path (team warp 0 of each tile): start, data ready, buffer ready, barrier, done; MMA sees A full
+st("decode: start -> data in smem (s14-s13)", diff(13, 14))
+st("decode: data -> buffer free (s0-s14)", diff(14, 0))
+m = n - 4
+prev_done = tr[2][:m]
+print("  tile: start, +data, +buf, +bar, +done | mma_afull_seen - done | gap to previous tile's MMA")
+for i in range(60, 72):
+    print("   %3d: %7d %+6d %+6d %+6d %+6d | %+6d" % (i, tr[13][i] - base, tr[14][i] - tr[13][i], tr[0][i] - tr[14][i],
+          tr[1][i] - tr[0][i], tr[2][i] - tr[1][i], tr[4][i] - tr[2][i]))
