@@ -110,6 +110,22 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the SpMM kernel from the newest committed ncu --set full
+    summary (profiles/*_ncu_*.json, written by tools/ncu_summary.py), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_*.json")), key=os.path.getmtime)
+    if not files:
+        return None
+    try:
+        with open(files[-1]) as f:
+            d = json.load(f)
+        return {"dram_bytes_per_launch": d["dram_bytes_per_launch"], "alg_bytes_per_launch": d["alg_bytes_per_launch"],
+                "cell": d.get("cell", ""), "source": os.path.relpath(files[-1], ROOT)}
+    except Exception:
+        return None
+
+
 def alg_bytes(t, n):
     return 4 * t.n_entries + 4 * (t.num_tiles + 1) + 2 * t.k * n + 4 * t.m * n
 
@@ -286,6 +302,7 @@ def run_ours(args, rank, world):
     if world == 1 and not args.no_e2e:
         e2e = run_e2e(args, tc, mats, xs, cells, dev)
 
+    traffic = ncu_traffic()
     result = {
         "metric": METRIC,
         "value": round(flops / (ms * 1e-3) / 1e12, 3),
@@ -308,7 +325,8 @@ def run_ours(args, rank, world):
         "hbm_gbs": round(total_alg / (ms * 1e-3) / 1e9, 1),
         "roofline": {"bound": "hbm", "achieved": round(sum_bytes / sum_t / 1e3, 1), "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(sum_bytes / sum_t / 1e3 / hbm_peak, 3),
-                     "traffic": None, "peak_kind": peak_kind,
+                     "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                     "traffic_detail": traffic, "peak_kind": peak_kind,
                      "kernel": "tcsl spmm_sm100_kernel (+ split-K reduce when split>1)",
                      "bytes_per_launch": "4E + 4(T+1) + 2KN + 4MN",
                      # time-weighted fraction of max(t_HBM, t_TC) (tensor-bound cells included)
