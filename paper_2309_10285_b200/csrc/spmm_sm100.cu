@@ -59,14 +59,25 @@ constexpr int kMTB = 128, kKTB = 64;
 constexpr uint32_t kABytes = kMTB * kKTB * 2;  // dense fp16 tile, 16 KB
 constexpr int kTeams = 5;                      // decode teams
 constexpr int kTeamWarps = 4;                  // warps per team
-constexpr int kNA = kTeams;                    // dense-tile buffers (one per team)
+constexpr int kBufPerTeam = 1;                 // 2: a team decodes its next tile while the MMA still
+                                               // reads its previous one (costs a second address set)
+constexpr int kNA = kBufPerTeam * kTeams;      // dense-tile buffers
 constexpr int kGMax = 20;                      // groups per warp per tile remembered for re-clearing
 constexpr int kWarpEpi = kTeams * kTeamWarps;  // epilogue warps 20 .. 23 (id % 4 = TMEM lane quarter)
 constexpr int kWarpStream = kWarpEpi + 4;      // entry stream: bulk copies only (blocking waits)
-constexpr int kWarpPoll = kWarpStream + 1;     // polling warp: tile metadata, X stages, epilogue wake-ups
+constexpr int kWarpX = kWarpStream + 1;        // X stages (TMA; blocking waits)
+constexpr int kWarpPoll = kWarpX + 1;          // polling warp: tile metadata, epilogue wake-ups (no TMA)
 constexpr int kWarpMma = kWarpPoll + 1;
 constexpr int kThreads = 32 * (kWarpMma + 1);  // 864
-constexpr int kBarEpi = 1 + kTeams;            // named barriers 1..kTeams: teams; then 2 for epilogue wake-ups
+constexpr int kBarEpi = 1 + kTeams;            // named barriers 1..kTeams: teams; then 2 for epilogue wake-ups,
+constexpr int kBarBuf = kBarEpi + 2;           // then kNA buffer-release wake-ups (the polling warp turns the
+                                               // MMA's aempty commits into named-barrier arrivals)
+static_assert(kBarBuf + kNA <= 16, "named barriers");
+// The MMA issuer waits once per kG tiles (one try_wait costs ~120-160 cycles
+// even when the phase is complete, profiles/r01_mma_loop_bench.txt): afull /
+// aempty are per group of kG consecutive buffers.
+constexpr int kG = (kNA % 2 == 0) ? 2 : 1;
+constexpr int kNP = kNA / kG;
 constexpr uint32_t kRing = 65536;              // entry ring bytes (power of two)
 constexpr uint32_t kChunk = 16384;             // bytes per bulk copy (>= 8 KB: ~7 TB/s, profiles/r01_bulk_copy_bench.txt)
 constexpr int kNR = kRing / kChunk;            // chunks in flight
@@ -88,7 +99,7 @@ struct Cfg {
   static constexpr int kTX = NH <= 32 ? 4 : (NH == 64 ? 2 : 1);  // k-tiles per X stage (TMA box <= 256 rows)
   static constexpr uint32_t kBoxBytes = 64u * kTX * kBoxW * 2;
   static constexpr uint32_t kXStage = kBoxBytes * kBoxes;
-  static constexpr int kNX = (49152 / kXStage) < 2 ? 2 : ((49152 / kXStage) > 4 ? 4 : (49152 / kXStage));
+  static constexpr int kNX = (32768 / kXStage) < 2 ? 2 : ((32768 / kXStage) > 4 ? 4 : (32768 / kXStage));
   static constexpr uint32_t kRowBytes = kBoxW * 2;
   static constexpr uint32_t kLayout = kRowBytes == 16 ? 0u : (kRowBytes == 32 ? 6u : (kRowBytes == 64 ? 4u : 2u));
   // SWIZZLE_NONE (16-B rows): LBO = k-group stride (8 rows x 16 B); swizzled: SBO =
@@ -108,8 +119,9 @@ struct Cfg {
   static constexpr uint32_t kOffSmall = kRing;
   static constexpr uint32_t kOffX = kOffSmall + kSmallBytes;  // 1 KB aligned
   static constexpr uint32_t kEndX = kOffX + kNX * kXStage;
-  static constexpr uint32_t kOffA = ((kEndX + 1024 + 16383) & ~16383u) - 1024;  // assuming B % 16 KB == 1 KB
+  static constexpr uint32_t kOffA = kEndX;  // 1 KB aligned
   static constexpr uint32_t kSmem = kOffA + kNA * kABytes;
+  static_assert(kSmem <= 227u * 1024u, "shared memory budget");
 };
 
 struct Params {
@@ -139,9 +151,13 @@ __device__ unsigned* g_hb = nullptr;
 #else
 #define HB(state, v) do { } while (0)
 #endif
-// Ablation switches for performance experiments (env TCSL_DEBUG, read once per
-// process; 0 in production): 1 skip scatter+clear, 2 skip MMAs, 4 skip ring loads.
+// Ablation switches for performance experiments, TCSL_TRACE builds only (env
+// TCSL_DEBUG): 1 skip scatter+clear, 2 skip MMAs, 4 skip ring loads.
+#ifdef TCSL_TRACE
 #define DBG(bit) (p.dbg & (bit))
+#else
+#define DBG(bit) 0
+#endif
 #ifdef TCSL_TRACE
 #define TRACE(slot, idx) \
   do { if (blockIdx.x == 0 && p.trace && (idx) < 4096) p.trace[(slot) * 4096 + (idx)] = clock64(); } while (0)
@@ -162,13 +178,13 @@ __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
 }
 
 // Byte offset of tile element `loc` (= x*64 + y) in the K-major SWIZZLE_NONE
-// canonical layout: (x/8)*1024 + (y/8)*128 + (x%8)*16 + (y%8)*2, OR-ed into the
-// 16 KB-aligned tile base. Bits >= 13 of loc are ignored, so the address is
-// always inside the tile.
+// canonical layout: (x/8)*1024 + (y/8)*128 + (x%8)*16 + (y%8)*2, added to the
+// tile base. Bits >= 13 of loc are ignored, so the address is always inside
+// the tile.
 __device__ __forceinline__ uint32_t a_addr(uint32_t a_tile, uint32_t loc) {
-  return (((loc << 1) & 0x3C0Eu) | a_tile)  // (y%8)*2 from loc[2:0], (x/8)*1024 from loc[12:9]
-         | ((loc >> 2) & 0x70u)            // (x%8)*16 from loc[8:6]
-         | ((loc << 4) & 0x380u);          // (y/8)*128 from loc[5:3]
+  return a_tile + (((loc << 1) & 0x3C0Eu)   // (y%8)*2 from loc[2:0], (x/8)*1024 from loc[12:9]
+                   | ((loc >> 2) & 0x70u)   // (x%8)*16 from loc[8:6]
+                   | ((loc << 4) & 0x380u));  // (y/8)*128 from loc[5:3]
 }
 
 __device__ __forceinline__ void st_shared_u32(uint32_t addr, uint32_t v) {
@@ -260,8 +276,8 @@ __device__ __forceinline__ void release_ring(const Smem& s, uint32_t lo, uint32_
 // One decode warp's part of tile gt (see the file comment). Z / nz describe
 // what this warp last wrote into the tile's buffer.
 __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint32_t gt, int team, int tw, int lane,
-                                            uint32_t afull_leader, uint32_t (&E)[kGMax], uint32_t (&Z)[kGMax],
-                                            uint32_t& nz, uint32_t& err_or) {
+                                            uint32_t afull_leader, uint32_t total, uint32_t (&E)[kGMax],
+                                            uint32_t (&Z)[kGMax], uint32_t& nz, uint32_t& err_or) {
   // per-tile metadata from the stream producer (normally published long ago)
   HB(1, gt);
   if (tw == 0 && lane == 0) TRACE(13, gt);
@@ -273,7 +289,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
     }
   }
   const uint2 meta = lds64(s.meta + 8 * (gt % kMeta));  // (stream offset, groups)
-  const uint32_t g0w = (meta.y * tw) >> 2, g1w = (meta.y * (tw + 1)) >> 2;
+  const uint32_t g0w = meta.y * tw / kTeamWarps, g1w = meta.y * (tw + 1) / kTeamWarps;
   const uint32_t cnt = g1w - g0w;
   const uint32_t ncnt = min(cnt, static_cast<uint32_t>(kGMax));
   const uint32_t lo = meta.x + g0w * 128u, hi = meta.x + g1w * 128u;  // this warp's stream bytes
@@ -294,7 +310,8 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
 #pragma unroll
     for (int j = 0; j < kGMax; ++j) err_or |= E[j];
     // the entries are in registers now (err_or consumed them): hand the ring
-    // bytes back at once so the stream refills while this tile is scattered
+    // bytes back at once so the stream refills while this tile waits for its
+    // buffer (holding them longer starves the ring at low sparsity)
     __syncwarp();
     if (cnt <= static_cast<uint32_t>(kGMax) && lane == 0) release_ring(s, lo, hi);
   }
@@ -302,15 +319,16 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   const uint32_t b = gt % kNA;
   const uint32_t a_tile = s.a + b * kABytes;
   HB(3, gt);
-  if (gt >= static_cast<uint32_t>(kNA)) mbar_wait_backoff(s.aempty + 8 * b, ((gt / kNA) - 1) & 1, 64);
+  // buffer b free again: the MMA of tile gt - kNA has completed. The polling
+  // warp observed that commit and arrives here; waiting on a named barrier
+  // costs no issue slots and no sync-unit polling.
+  if (gt >= static_cast<uint32_t>(kNA)) named_bar_sync(kBarBuf + b, (kTeamWarps + 1) * 32);
   if (tw == 0 && lane == 0) TRACE(0, gt);
   HB(4, gt);
   // s.ovf[b] = the last tile in buffer b for which some warp of the team wrote
-  // more groups than it remembers: then the whole team clears by quarters.
+  // more groups than it remembers: then the whole team zeroes the tile.
   if (gt >= static_cast<uint32_t>(kNA) && lds32(s.ovf + 4 * b) == gt - kNA) {
-    const uint32_t q0 = a_tile + tw * (kABytes / kTeamWarps);
-#pragma unroll
-    for (int r = 0; r < static_cast<int>(kABytes / kTeamWarps / 512); ++r) sts128_zero(q0 + 512 * r + 16 * lane);
+    for (int r = tw; r < static_cast<int>(kABytes / 512); r += kTeamWarps) sts128_zero(a_tile + 512 * r + 16 * lane);
   } else if (!DBG(1)) {
     clear_groups(Z, nz);
   }
@@ -331,19 +349,25 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
     }
     if (lane == 0) st_shared_u32(s.ovf + 4 * b, gt);
   }
+  if (cnt > static_cast<uint32_t>(kGMax) && lane == 0) release_ring(s, lo, hi);  // overflowed: read the ring until now
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
     // signal the MMA (an overflowed warp hands its ring bytes back only now)
-    if (cnt > static_cast<uint32_t>(kGMax)) release_ring(s, lo, hi);
-    mbar_arrive_cluster(afull_leader + 8 * b);
+    // a trailing group with fewer than kG tiles: arrive for the missing ones too
+    const uint32_t ab = afull_leader + 8 * (b / kG);
+    const uint32_t missing = (gt % kG == 0 && gt + kG > total) ? gt + kG - total : 0u;
+    if (missing)
+      asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0], %1;" ::"r"(ab), "r"(missing + 1) : "memory");
+    else
+      mbar_arrive_cluster(ab);
   }
   if (tw == 0 && lane == 0) TRACE(2, gt);
   HB(7, gt);
 }
 
 template <int NH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
     spmm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
   using C = Cfg<NH>;
   constexpr int NX = C::kNX;
@@ -352,13 +376,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   Smem s;
   s.ring = opaque(base + C::kOffRing);
   s.x = opaque(base + C::kOffX);
-  s.a = opaque(((base + C::kOffA) + 16383u) & ~16383u);  // == base + kOffA when base % 16 KB == 1 KB
+  s.a = opaque(base + C::kOffA);
   const uint32_t sm = base + C::kOffSmall;
   s.cfull = opaque(sm);              // [kNB] ring chunk landed (bulk-copy bytes)
   s.cempty = s.cfull + 8 * kNB;      // [kNR] ring chunk consumed (decoders' complete_tx bytes)
-  s.afull = s.cempty + 8 * kNR;      // [kNA] even CTA: 8 arrivals (4 decode warps x 2 CTAs)
-  s.aempty = s.afull + 8 * kNA;      // [kNA] both CTAs: MMA commit
-  s.xfull = s.aempty + 8 * kNA;      // [NX] even CTA: 2 arrivals + both halves' bytes
+  s.afull = s.cempty + 8 * kNR;      // [kNP] even CTA: kG tiles x 4 decode warps x 2 CTAs arrivals
+  s.aempty = s.afull + 8 * kNP;      // [kNP] both CTAs: MMA commit after the group's last tile
+  s.xfull = s.aempty + 8 * kNP;      // [NX] even CTA: 2 arrivals + both halves' bytes
   s.xempty = s.xfull + 8 * NX;       // [NX] both CTAs: MMA commit
   s.dfull = s.xempty + 8 * NX;       // [2] both CTAs: MMA commit
   s.dempty = s.dfull + 16;           // [2] even CTA: 8 arrivals (4 epilogue warps x 2 CTAs)
@@ -371,7 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   s.done = s.tiles_ready + 4;        // tiles whose metadata the decoders have read
   s.tab_ready = s.done + 4;          // unit table written (stream warp -> polling warp)
   s.tmem_slot = s.tab_ready + 4;
-  static_assert(8 * (kNB + kNR + 2 * kNA + 2 * NX + 4 + kMeta) + 12 * kMaxUnits + 4 * kNA + 16 <= kSmallBytes,
+  static_assert(8 * (kNB + kNR + 2 * kNP + 2 * NX + 4 + kMeta) + 12 * kMaxUnits + 4 * kNA + 16 <= kSmallBytes,
                 "small smem region");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (s.tmem_slot - base));
 
@@ -382,12 +406,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int ncl = static_cast<int>(num_clusters_x());
 
   if (threadIdx.x == 0) {
-    if (s.a + kNA * kABytes > base + C::kSmem) __trap();  // dynamic smem not placed as assumed
     for (int i = 0; i < kNB; ++i) mbar_init(s.cfull + 8 * i, 1);
     for (int i = 0; i < kNR; ++i) mbar_init(s.cempty + 8 * i, 1);
     for (int i = 0; i < kNA; ++i) {
-      mbar_init(s.afull + 8 * i, 2 * kTeamWarps);
-      mbar_init(s.aempty + 8 * i, 1);
+      if (i < kNP) {
+        mbar_init(s.afull + 8 * i, kG * 2 * kTeamWarps);
+        mbar_init(s.aempty + 8 * i, 1);
+      }
       st_shared_u32(s.ovf + 4 * i, 0xFFFFFFFFu);
     }
     for (int i = 0; i < NX; ++i) {
@@ -403,7 +428,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     st_shared_u32(s.tab_ready, 0u);
     fence_barrier_init();
   }
-  if (warp == kWarpPoll && lane == 0) prefetch_tmap(&tmap_x);
+  if (warp == kWarpX && lane == 0) prefetch_tmap(&tmap_x);
   if (warp == kWarpMma) tmem_alloc_pair(s.tmem_slot, C::kTmemCols);
   for (uint32_t i = threadIdx.x; i < kNA * kABytes / 16; i += kThreads) sts128_zero(s.a + 16 * i);
   HB(60, 0);
@@ -424,13 +449,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       total += un.kt1 - un.kt0;
     }
     const uint32_t afull_leader = mapa_shared(s.afull, 0);
-    uint32_t E[kGMax], Z[kGMax];
+    uint32_t E[kGMax];
 #pragma unroll
     for (int j = 0; j < kGMax; ++j) E[j] = 0u;  // slots past a tile's count keep older, checked entries
-    uint32_t nz = 0;
     uint32_t err_or = 0;
-    for (uint32_t gt = team; gt < total; gt += kTeams)
-      decode_tile(p, s, gt, team, tw, lane, afull_leader, E, Z, nz, err_or);
+    if constexpr (kBufPerTeam == 2) {
+      uint32_t Z0[kGMax], Z1[kGMax];  // addresses last written to the team's two buffers
+      uint32_t n0 = 0, n1 = 0;
+      for (uint32_t gt = team; gt < total; gt += 2 * kTeams) {
+        decode_tile(p, s, gt, team, tw, lane, afull_leader, total, E, Z0, n0, err_or);
+        if (gt + kTeams < total) decode_tile(p, s, gt + kTeams, team, tw, lane, afull_leader, total, E, Z1, n1, err_or);
+      }
+    } else {
+      uint32_t Z[kGMax];  // addresses last written to the team's buffer
+      uint32_t nz = 0;
+      for (uint32_t gt = team; gt < total; gt += kTeams)
+        decode_tile(p, s, gt, team, tw, lane, afull_leader, total, E, Z, nz, err_or);
+    }
     // locations >= 8192 leave the 128x64 tile (the scatter masked them into range)
     if (__any_sync(0xffffffffu, (err_or & 0xE000u) != 0) && lane == 0)
       raise_dev(p.err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
@@ -550,26 +585,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     }
+  } else if (warp == kWarpX) {
+    // ---------------------------------------------------------------- X stages
+    // TMA loads of this CTA's half of the B columns, kTX k-tiles per stage; both
+    // halves complete on the even CTA's xfull barrier (.cta_group::2). A TMA
+    // issue can block behind the stream's bulk copies, hence its own warp.
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_last();
+      const uint32_t xfull_leader = mapa_shared(s.xfull, 0);
+      uint32_t gs = 0;  // X stage counter
+      for (int u = cid; u < p.units; u += ncl) {
+        const Unit un = unit_of(p, u);
+        for (int kt = un.kt0; kt < un.kt1; kt += C::kTX, ++gs) {
+          const uint32_t slot = gs % NX;
+          if (gs >= static_cast<uint32_t>(NX)) mbar_wait(s.xempty + 8 * slot, ((gs / NX) - 1) & 1);
+          mbar_arrive_expect_tx_cluster(xfull_leader + 8 * slot, C::kXStage);
+#pragma unroll
+          for (int bx = 0; bx < C::kBoxes; ++bx)
+            tma_load_2d_pair(s.x + slot * C::kXStage + bx * C::kBoxBytes, &tmap_x,
+                             p.col0 + static_cast<int>(rank) * NH + bx * C::kBoxW, kt * kKTB, xfull_leader + 8 * slot,
+                             pol);
+          TRACE(5, gs);
+        }
+      }
+    }
   } else if (warp == kWarpPoll) {
     // ---------------------------------------------------------------- polling warp
-    // Non-blocking checks only (mbarrier.test_wait): (a) per-tile metadata
-    // (stream offset, groups), 32 tiles per step, one lane per tile, offsets
-    // loaded one step ahead; (b) X stages (TMA, this CTA's half of the B
-    // columns); (c) epilogue wake-ups (named barrier per accumulator).
-    uint32_t nunits = 0, ntiles = 0, nstages = 0;
+    // Non-blocking checks only (mbarrier.test_wait), no TMA issue: (a) per-tile
+    // metadata (stream offset, groups), 32 tiles per step, one lane per tile,
+    // offsets loaded one step ahead; (c) epilogue wake-ups (named barrier per
+    // accumulator).
+    uint32_t nunits = 0, ntiles = 0;
     for (int u = cid; u < p.units; u += ncl, ++nunits) {
       const Unit un = unit_of(p, u);
       ntiles += un.kt1 - un.kt0;
-      nstages += (un.kt1 - un.kt0 + C::kTX - 1) / C::kTX;
     }
-    const uint64_t pol_x = policy_evict_last();
-    const uint32_t xfull_leader = mapa_shared(s.xfull, 0);
     uint32_t gt = 0, mu = 0, mkt = 0;  // (a) next tile to publish: unit ordinal, k-tile within the unit
     int mu_id = cid;
     uint32_t pend = 0, pa0 = 0, pa1 = 0;  //     prefetched batch: tile count, this lane's offsets
-    uint32_t gs = 0, xkt = 0;          // (b) next X stage; its first k-tile within the unit
-    int xu_id = cid;
     uint32_t eu = 0;                   // (c) next unit whose accumulator the epilogue waits for
+    uint32_t rel = 0;                  // (d) next tile whose MMA completion releases its buffer
     auto prefetch_batch = [&]() {
       const Unit un = unit_of(p, mu_id);
       const int rb = 2 * un.rp + static_cast<int>(rank);
@@ -584,34 +639,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (ntiles) prefetch_batch();
     bool tab = false;
     long long idle_t0 = clock64();
-    while (gt < ntiles || gs < nstages || eu < nunits) {
+    while (gt < ntiles || eu < nunits || rel < ntiles) {
       bool progress = false;
-      if (lane == 0) {
-        // (b) X stages
-        while (gs < nstages && (gs < static_cast<uint32_t>(NX) || mbar_test_wait(s.xempty + 8 * (gs % NX), ((gs / NX) - 1) & 1))) {
-          const Unit un = unit_of(p, xu_id);
-          const uint32_t slot = gs % NX;
-          mbar_arrive_expect_tx_cluster(xfull_leader + 8 * slot, C::kXStage);
-#pragma unroll
-          for (int bx = 0; bx < C::kBoxes; ++bx)
-            tma_load_2d_pair(s.x + slot * C::kXStage + bx * C::kBoxBytes, &tmap_x,
-                             p.col0 + static_cast<int>(rank) * NH + bx * C::kBoxW,
-                             (un.kt0 + static_cast<int>(xkt)) * kKTB, xfull_leader + 8 * slot, pol_x);
-          TRACE(5, gs);
-          ++gs;
-          xkt += C::kTX;
-          if (xkt >= static_cast<uint32_t>(un.kt1 - un.kt0)) {
-            xkt = 0;
-            xu_id += ncl;
-          }
-          progress = true;
-        }
+      // (d) buffer releases: the MMA of tile rel committed -> wake the team that
+      //     decodes tile rel + kNA into the same buffer
+      //     (commits come per group of kG buffers: rel is a multiple of kG)
+      while (rel < ntiles &&
+             __shfl_sync(0xffffffffu, mbar_test_wait(s.aempty + 8 * ((rel % kNA) / kG), (rel / kNA) & 1) ? 1 : 0, 0)) {
+        if (lane == 0) TRACE(15, rel / kG);
+        for (uint32_t t = rel; t < rel + kG && t + kNA < ntiles; ++t)
+          asm volatile("bar.arrive %0, %1;" ::"r"(kBarBuf + (t % kNA)), "r"((kTeamWarps + 1) * 32) : "memory");
+        rel += kG;
+        progress = true;
       }
-      // lane 0 advanced gs / xkt / xu_id: broadcast (warp-uniform loop state)
-      progress = __shfl_sync(0xffffffffu, progress, 0);
-      gs = __shfl_sync(0xffffffffu, gs, 0);
-      xkt = __shfl_sync(0xffffffffu, xkt, 0);
-      xu_id = __shfl_sync(0xffffffffu, xu_id, 0);
       // (c) epilogue wake-ups (the whole warp arrives on the named barrier)
       while (eu < nunits && __shfl_sync(0xffffffffu, mbar_test_wait(s.dfull + 8 * (eu & 1), (eu >> 1) & 1) ? 1 : 0, 0)) {
         asm volatile("bar.arrive %0, %1;" ::"r"(kBarEpi + (eu & 1)), "r"(5 * 32) : "memory");
@@ -654,8 +694,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       if (progress) {
         idle_t0 = clock64();
-      } else if (clock64() - idle_t0 > 40000000000LL) {
-        __trap();  // watchdog, as in mbar_wait
+      } else {
+        // idle: back off so the polls do not crowd the sync unit the MMA issuer uses
+        __nanosleep(64);
+        if (clock64() - idle_t0 > 40000000000LL) __trap();  // watchdog, as in mbar_wait
       }
     }
   } else if (warp == kWarpMma && rank == 0) {
@@ -663,6 +705,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // The whole warp walks the schedule; one elected lane issues.
     const uint64_t a_desc0 = smem_desc(s.a, 128, 1024, 0);
     const uint64_t b_desc0 = smem_desc(s.x, C::kLBO, C::kSBO, C::kLayout);
+    uint32_t total = 0;  // k-tiles of this CTA
+    for (int u = cid; u < p.units; u += ncl) {
+      const Unit un = unit_of(p, u);
+      total += un.kt1 - un.kt0;
+    }
     uint32_t gt = 0, ui = 0, gs = 0;
     for (int u = cid; u < p.units; u += ncl, ++ui) {
       const Unit un = unit_of(p, u);
@@ -678,9 +725,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (in_stage == 0) mbar_wait_cluster(s.xfull + 8 * xs, (gs / NX) & 1);
         const uint32_t b = gt % kNA;
         if (lane == 0) TRACE(3, gt);
-        HB(41, gt);
-        mbar_wait_cluster(s.afull + 8 * b, (gt / kNA) & 1);
-        HB(42, gt);
+        if (gt % kG == 0) mbar_wait_cluster(s.afull + 8 * (b / kG), (gt / kNA) & 1);  // all tiles of the group
         if (lane == 0) TRACE(4, gt);
         tc_fence_after();
         const uint64_t ad = a_desc0 + ((b * kABytes) >> 4);
@@ -692,7 +737,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (!DBG(2))
               mma_f16_ss_pair(d_tmem, ad + (k4 * 256 >> 4), bd + (k4 * C::kKStep >> 4), C::kIdesc,
                               (kt > un.kt0 || k4 > 0) ? 1u : 0u);
-          mma_commit_pair(s.aempty + 8 * b, 3);
+          if (gt % kG == kG - 1 || gt + 1 == total) mma_commit_pair(s.aempty + 8 * (b / kG), 3);
+          TRACE(7, gt);
           if (stage_done) mma_commit_pair(s.xempty + 8 * xs, 3);
         }
         __syncwarp();

@@ -57,34 +57,18 @@ def diff(a, b):
     return (tr[b] - tr[a])[m][2:-2].astype(float)
 
 
-st("decode: buffer ready -> team barrier passed (s1-s0)", diff(0, 1))
-st("decode: barrier -> tile done (s2-s1)", diff(1, 2))
-d0 = tr[0][:n][tr[0][:n] != 0]
-st("decode: team-tile period (team of tile 0)", np.diff(d0[::3]).astype(float)[1:-1])
-st("mma: wait A full (s4-s3)", diff(3, 4))
-m3 = tr[3][:n].astype(float)
-st("mma: tile period (s3[i+1]-s3[i])", np.diff(m3)[2:-2])
-st("decode done -> mma sees it (s4 - s2)", diff(2, 4))
-print(f"  tiles traced {n}, total cycles {tr[4][n - 1] - tr[3][0]}")
-st("mma: wait X stage (s3 - s8)", diff(8, 3))
 base = tr[8][0]
-xs = tr[5][tr[5] != 0] - base
-ch = tr[6][tr[6] != 0] - base
-print("  X stage issue times (cycles from first MMA poll):", xs[:12].tolist())
-print("  MMA tile-start times:", (tr[8][:48:4] - base).tolist())
-print("  chunk issue times:", ch[:24].tolist())
-print("  decode tile-ready times (s0):", (tr[0][:24] - base).tolist())
-it = tr[9][tr[9] != 0] - base
-print("  poller: pass-1 start", tr[12][0] - base, "loop start", tr[11][0] - base, "iterations traced", it.size)
-print("  poller iteration times:", it[:40].tolist())
-print("  poller iteration period p50", float(np.median(np.diff(it))) if it.size > 2 else None)
-print("  meta publish times (per 32 tiles):", (tr[10][:8] - base).tolist())
-# per-tile critical path (team warp 0 of each tile): start, data ready, buffer ready, barrier, done; MMA sees A full
-st("decode: start -> data in smem (s14-s13)", diff(13, 14))
-st("decode: data -> buffer free (s0-s14)", diff(14, 0))
-m = n - 4
-prev_done = tr[2][:m]
-print("  tile: start, +data, +buf, +bar, +done | mma_afull_seen - done | gap to previous tile's MMA")
-for i in range(60, 72):
-    print("   %3d: %7d %+6d %+6d %+6d %+6d | %+6d" % (i, tr[13][i] - base, tr[14][i] - tr[13][i], tr[0][i] - tr[14][i],
-          tr[1][i] - tr[0][i], tr[2][i] - tr[1][i], tr[4][i] - tr[2][i]))
+
+
+def d(a, b, i):
+    return int(tr[b][i] - tr[a][i]) if tr[a][i] and tr[b][i] else None
+print("  tile | start +data +buf +bar +done | mma: +afull_seen(after done) +issued | release(pair) after issue")
+for i in range(100, 116):
+    rel = int(tr[15][i // 2] - tr[7][i | 1]) if tr[15][i // 2] and tr[7][i | 1] else None
+    print("  %4d | %7d %+5s %+5s %+5s %+5s | %+6s %+5s | %+6s" % (i, tr[13][i] - base, d(13, 14, i), d(14, 0, i), d(0, 1, i),
+          d(1, 2, i), d(2, 4, i), d(4, 7, i), rel))
+st("mma: iteration (s8[i+1]-s8[i])", np.diff(tr[8][:n].astype(float))[2:-2])
+st("decode: start->data", diff(13, 14))
+st("decode: data->buffer", diff(14, 0))
+st("decode: buffer->barrier", diff(0, 1))
+st("decode: barrier->done", diff(1, 2))
