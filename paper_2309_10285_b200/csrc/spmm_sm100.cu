@@ -57,27 +57,41 @@ namespace {
 
 constexpr int kMTB = 128, kKTB = 64;
 constexpr uint32_t kABytes = kMTB * kKTB * 2;  // dense fp16 tile, 16 KB
-constexpr int kTeams = 5;                      // decode teams
-constexpr int kTeamWarps = 4;                  // warps per team
-constexpr int kBufPerTeam = 1;                 // 2: a team decodes its next tile while the MMA still
-                                               // reads its previous one (costs a second address set)
-constexpr int kNA = kBufPerTeam * kTeams;      // dense-tile buffers
 constexpr int kGMax = 20;                      // groups per warp per tile remembered for re-clearing
-constexpr int kWarpEpi = kTeams * kTeamWarps;  // epilogue warps 20 .. 23 (id % 4 = TMEM lane quarter)
-constexpr int kWarpStream = kWarpEpi + 4;      // entry stream: bulk copies only (blocking waits)
-constexpr int kWarpX = kWarpStream + 1;        // X stages (TMA; blocking waits)
-constexpr int kWarpPoll = kWarpX + 1;          // polling warp: tile metadata, epilogue wake-ups (no TMA)
-constexpr int kWarpMma = kWarpPoll + 1;
-constexpr int kThreads = 32 * (kWarpMma + 1);  // 864
-constexpr int kBarEpi = 1 + kTeams;            // named barriers 1..kTeams: teams; then 2 for epilogue wake-ups,
-constexpr int kBarBuf = kBarEpi + 2;           // then kNA buffer-release wake-ups (the polling warp turns the
-                                               // MMA's aempty commits into named-barrier arrivals)
-static_assert(kBarBuf + kNA <= 16, "named barriers");
-// The MMA issuer waits once per kG tiles (one try_wait costs ~120-160 cycles
-// even when the phase is complete, profiles/r01_mma_loop_bench.txt): afull /
-// aempty are per group of kG consecutive buffers.
-constexpr int kG = (kNA % 2 == 0) ? 2 : 1;
-constexpr int kNP = kNA / kG;
+
+// Decode team shape. One dense-tile buffer per team. T teams of W warps; the
+// host picks the shape from the matrix's mean groups per tile (spmm_team_shape):
+// sparse tiles are decoded by 2-warp teams (half the per-tile bookkeeping, 8
+// tiles in flight), denser ones by 4-warp teams (each warp's share of a tile
+// must fit the kGMax remembered addresses).
+template <int T, int W>
+struct Teams {
+  static constexpr int kTeams = T;
+  static constexpr int kTeamWarps = W;
+  static constexpr int kNA = T;                    // dense-tile buffers (one per team)
+  // The MMA issuer waits once per kG tiles (one try_wait costs ~120-160 cycles
+  // even when the phase is complete, profiles/r01_mma_loop_bench.txt): afull /
+  // aempty are per group of kG consecutive buffers.
+  static constexpr int kG = (kNA % 2 == 0) ? 2 : 1;
+  static constexpr int kNP = kNA / kG;
+  static constexpr int kWarpEpi = T * W;           // 4 epilogue warps (id % 4 = TMEM lane quarter)
+  static constexpr int kWarpStream = kWarpEpi + 4;  // entry stream: bulk copies only (blocking waits)
+  static constexpr int kWarpX = kWarpStream + 1;   // X stages (TMA; blocking waits)
+  static constexpr int kWarpPoll = kWarpX + 1;     // polling warp: tile metadata, wake-ups (no TMA)
+  static constexpr int kWarpMma = kWarpPoll + 1;
+  static constexpr int kThreads = 32 * (kWarpMma + 1);
+  // Named barrier 1 + t serves team t twice per tile: the buffer-release wake-up
+  // (W warps + the polling warp, which arrives once the MMA of the buffer's
+  // previous tile has committed) and then the team barrier (W warps). The next
+  // release can only follow that tile's MMA, i.e. after the team barrier phase.
+  static constexpr int kBarEpi = 1 + T;            // 2 epilogue wake-ups (per accumulator)
+  static_assert(kBarEpi + 2 <= 16, "named barriers");
+  // Register file per SMSP: ceil(warps / 4) * 32 * regs <= 16384.
+  static constexpr int kMaxRegs = ((16384 / (32 * ((kWarpMma + 1 + 3) / 4))) / 8) * 8;
+};
+using TeamsSparse = Teams<8, 2>;
+using TeamsDense = Teams<5, 4>;
+
 constexpr uint32_t kRing = 65536;              // entry ring bytes (power of two)
 constexpr uint32_t kChunk = 16384;             // bytes per bulk copy (>= 8 KB: ~7 TB/s, profiles/r01_bulk_copy_bench.txt)
 constexpr int kNR = kRing / kChunk;            // chunks in flight
@@ -91,7 +105,7 @@ constexpr int kMeta = 64;                      // per-tile metadata ring (stream
 constexpr uint32_t kSmallBytes = 3072;         // barriers + tables (see Smem)
 
 // NH = B columns held by each CTA of the pair (the MMA's N is 2 * NH).
-template <int NH>
+template <int NH, int NA>
 struct Cfg {
   static constexpr int kN = 2 * NH;
   static constexpr int kBoxW = NH < 64 ? NH : 64;  // TMA box / swizzle atom width
@@ -120,7 +134,7 @@ struct Cfg {
   static constexpr uint32_t kOffX = kOffSmall + kSmallBytes;  // 1 KB aligned
   static constexpr uint32_t kEndX = kOffX + kNX * kXStage;
   static constexpr uint32_t kOffA = kEndX;  // 1 KB aligned
-  static constexpr uint32_t kSmem = kOffA + kNA * kABytes;
+  static constexpr uint32_t kSmem = kOffA + NA * kABytes;
   static_assert(kSmem <= 227u * 1024u, "shared memory budget");
 };
 
@@ -275,6 +289,7 @@ __device__ __forceinline__ void release_ring(const Smem& s, uint32_t lo, uint32_
 
 // One decode warp's part of tile gt (see the file comment). Z / nz describe
 // what this warp last wrote into the tile's buffer.
+template <class TM>
 __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint32_t gt, int team, int tw, int lane,
                                             uint32_t afull_leader, uint32_t total, uint32_t (&E)[kGMax],
                                             uint32_t (&Z)[kGMax], uint32_t& nz, uint32_t& err_or) {
@@ -289,7 +304,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
     }
   }
   const uint2 meta = lds64(s.meta + 8 * (gt % kMeta));  // (stream offset, groups)
-  const uint32_t g0w = meta.y * tw / kTeamWarps, g1w = meta.y * (tw + 1) / kTeamWarps;
+  const uint32_t g0w = meta.y * tw / TM::kTeamWarps, g1w = meta.y * (tw + 1) / TM::kTeamWarps;
   const uint32_t cnt = g1w - g0w;
   const uint32_t ncnt = min(cnt, static_cast<uint32_t>(kGMax));
   const uint32_t lo = meta.x + g0w * 128u, hi = meta.x + g1w * 128u;  // this warp's stream bytes
@@ -316,24 +331,24 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
     if (cnt <= static_cast<uint32_t>(kGMax) && lane == 0) release_ring(s, lo, hi);
   }
   if (tw == 0 && lane == 0) TRACE(14, gt);
-  const uint32_t b = gt % kNA;
+  const uint32_t b = gt % TM::kNA;
   const uint32_t a_tile = s.a + b * kABytes;
   HB(3, gt);
-  // buffer b free again: the MMA of tile gt - kNA has completed. The polling
+  // buffer b free again: the MMA of tile gt - TM::kNA has completed. The polling
   // warp observed that commit and arrives here; waiting on a named barrier
   // costs no issue slots and no sync-unit polling.
-  if (gt >= static_cast<uint32_t>(kNA)) named_bar_sync(kBarBuf + b, (kTeamWarps + 1) * 32);
+  if (gt >= static_cast<uint32_t>(TM::kNA)) named_bar_sync(1 + team, (TM::kTeamWarps + 1) * 32);
   if (tw == 0 && lane == 0) TRACE(0, gt);
   HB(4, gt);
   // s.ovf[b] = the last tile in buffer b for which some warp of the team wrote
   // more groups than it remembers: then the whole team zeroes the tile.
-  if (gt >= static_cast<uint32_t>(kNA) && lds32(s.ovf + 4 * b) == gt - kNA) {
-    for (int r = tw; r < static_cast<int>(kABytes / 512); r += kTeamWarps) sts128_zero(a_tile + 512 * r + 16 * lane);
+  if (gt >= static_cast<uint32_t>(TM::kNA) && lds32(s.ovf + 4 * b) == gt - TM::kNA) {
+    for (int r = tw; r < static_cast<int>(kABytes / 512); r += TM::kTeamWarps) sts128_zero(a_tile + 512 * r + 16 * lane);
   } else if (!DBG(1)) {
     clear_groups(Z, nz);
   }
   HB(5, gt);
-  named_bar_sync(1 + team, kTeamWarps * 32);
+  named_bar_sync(1 + team, TM::kTeamWarps * 32);
   HB(6, gt);
   if (tw == 0 && lane == 0) {
     TRACE(1, gt);
@@ -354,9 +369,9 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   __syncwarp();
   if (lane == 0) {
     // signal the MMA (an overflowed warp hands its ring bytes back only now)
-    // a trailing group with fewer than kG tiles: arrive for the missing ones too
-    const uint32_t ab = afull_leader + 8 * (b / kG);
-    const uint32_t missing = (gt % kG == 0 && gt + kG > total) ? gt + kG - total : 0u;
+    // a trailing group with fewer than TM::kG tiles: arrive for the missing ones too
+    const uint32_t ab = afull_leader + 8 * (b / TM::kG);
+    const uint32_t missing = (gt % TM::kG == 0 && gt + TM::kG > total) ? gt + TM::kG - total : 0u;
     if (missing)
       asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0], %1;" ::"r"(ab), "r"(missing + 1) : "memory");
     else
@@ -366,10 +381,10 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   HB(7, gt);
 }
 
-template <int NH>
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
+template <int NH, class TM>
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
     spmm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
-  using C = Cfg<NH>;
+  using C = Cfg<NH, TM::kNA>;
   constexpr int NX = C::kNX;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t base = smem_u32(smem_raw);
@@ -380,9 +395,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
   const uint32_t sm = base + C::kOffSmall;
   s.cfull = opaque(sm);              // [kNB] ring chunk landed (bulk-copy bytes)
   s.cempty = s.cfull + 8 * kNB;      // [kNR] ring chunk consumed (decoders' complete_tx bytes)
-  s.afull = s.cempty + 8 * kNR;      // [kNP] even CTA: kG tiles x 4 decode warps x 2 CTAs arrivals
-  s.aempty = s.afull + 8 * kNP;      // [kNP] both CTAs: MMA commit after the group's last tile
-  s.xfull = s.aempty + 8 * kNP;      // [NX] even CTA: 2 arrivals + both halves' bytes
+  s.afull = s.cempty + 8 * kNR;      // [TM::kNP] even CTA: TM::kG tiles x 4 decode warps x 2 CTAs arrivals
+  s.aempty = s.afull + 8 * TM::kNP;      // [TM::kNP] both CTAs: MMA commit after the group's last tile
+  s.xfull = s.aempty + 8 * TM::kNP;      // [NX] even CTA: 2 arrivals + both halves' bytes
   s.xempty = s.xfull + 8 * NX;       // [NX] both CTAs: MMA commit
   s.dfull = s.xempty + 8 * NX;       // [2] both CTAs: MMA commit
   s.dempty = s.dfull + 16;           // [2] even CTA: 8 arrivals (4 epilogue warps x 2 CTAs)
@@ -390,12 +405,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
   s.tab_s = s.meta + 8 * kMeta;      // [kMaxUnits] unit table: stream offset of the unit
   s.tab_g0 = s.tab_s + 4 * kMaxUnits;  // offsets[first tile]
   s.tab_g1 = s.tab_g0 + 4 * kMaxUnits;  // offsets[last tile + 1] (== g0 for an invalid unit)
-  s.ovf = s.tab_g1 + 4 * kMaxUnits;  // [kNA]
-  s.tiles_ready = s.ovf + 4 * kNA;   // tiles with published metadata
+  s.ovf = s.tab_g1 + 4 * kMaxUnits;  // [TM::kNA]
+  s.tiles_ready = s.ovf + 4 * TM::kNA;   // tiles with published metadata
   s.done = s.tiles_ready + 4;        // tiles whose metadata the decoders have read
   s.tab_ready = s.done + 4;          // unit table written (stream warp -> polling warp)
   s.tmem_slot = s.tab_ready + 4;
-  static_assert(8 * (kNB + kNR + 2 * kNP + 2 * NX + 4 + kMeta) + 12 * kMaxUnits + 4 * kNA + 16 <= kSmallBytes,
+  static_assert(8 * (kNB + kNR + 2 * TM::kNP + 2 * NX + 4 + kMeta) + 12 * kMaxUnits + 4 * TM::kNA + 16 <= kSmallBytes,
                 "small smem region");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (s.tmem_slot - base));
 
@@ -408,9 +423,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNB; ++i) mbar_init(s.cfull + 8 * i, 1);
     for (int i = 0; i < kNR; ++i) mbar_init(s.cempty + 8 * i, 1);
-    for (int i = 0; i < kNA; ++i) {
-      if (i < kNP) {
-        mbar_init(s.afull + 8 * i, kG * 2 * kTeamWarps);
+    for (int i = 0; i < TM::kNA; ++i) {
+      if (i < TM::kNP) {
+        mbar_init(s.afull + 8 * i, TM::kG * 2 * TM::kTeamWarps);
         mbar_init(s.aempty + 8 * i, 1);
       }
       st_shared_u32(s.ovf + 4 * i, 0xFFFFFFFFu);
@@ -428,9 +443,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
     st_shared_u32(s.tab_ready, 0u);
     fence_barrier_init();
   }
-  if (warp == kWarpX && lane == 0) prefetch_tmap(&tmap_x);
-  if (warp == kWarpMma) tmem_alloc_pair(s.tmem_slot, C::kTmemCols);
-  for (uint32_t i = threadIdx.x; i < kNA * kABytes / 16; i += kThreads) sts128_zero(s.a + 16 * i);
+  if (warp == TM::kWarpX && lane == 0) prefetch_tmap(&tmap_x);
+  if (warp == TM::kWarpMma) tmem_alloc_pair(s.tmem_slot, C::kTmemCols);
+  for (uint32_t i = threadIdx.x; i < TM::kNA * kABytes / 16; i += TM::kThreads) sts128_zero(s.a + 16 * i);
   HB(60, 0);
   fence_proxy_async_smem();
   tc_fence_before();
@@ -439,10 +454,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
   HB(61, 0);
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < kWarpEpi) {
+  if (warp < TM::kWarpEpi) {
     // ---------------------------------------------------------------- decode teams
-    const int team = warp / kTeamWarps;
-    const int tw = warp % kTeamWarps;
+    const int team = warp / TM::kTeamWarps;
+    const int tw = warp % TM::kTeamWarps;
     uint32_t total = 0;  // k-tiles of this CTA
     for (int u = cid; u < p.units; u += ncl) {
       const Unit un = unit_of(p, u);
@@ -453,23 +468,14 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
 #pragma unroll
     for (int j = 0; j < kGMax; ++j) E[j] = 0u;  // slots past a tile's count keep older, checked entries
     uint32_t err_or = 0;
-    if constexpr (kBufPerTeam == 2) {
-      uint32_t Z0[kGMax], Z1[kGMax];  // addresses last written to the team's two buffers
-      uint32_t n0 = 0, n1 = 0;
-      for (uint32_t gt = team; gt < total; gt += 2 * kTeams) {
-        decode_tile(p, s, gt, team, tw, lane, afull_leader, total, E, Z0, n0, err_or);
-        if (gt + kTeams < total) decode_tile(p, s, gt + kTeams, team, tw, lane, afull_leader, total, E, Z1, n1, err_or);
-      }
-    } else {
-      uint32_t Z[kGMax];  // addresses last written to the team's buffer
-      uint32_t nz = 0;
-      for (uint32_t gt = team; gt < total; gt += kTeams)
-        decode_tile(p, s, gt, team, tw, lane, afull_leader, total, E, Z, nz, err_or);
-    }
+    uint32_t Z[kGMax];  // addresses last written to the team's buffer
+    uint32_t nz = 0;
+    for (uint32_t gt = team; gt < total; gt += TM::kTeams)
+      decode_tile<TM>(p, s, gt, team, tw, lane, afull_leader, total, E, Z, nz, err_or);
     // locations >= 8192 leave the 128x64 tile (the scatter masked them into range)
     if (__any_sync(0xffffffffu, (err_or & 0xE000u) != 0) && lane == 0)
       raise_dev(p.err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
-  } else if (warp < kWarpEpi + 4) {
+  } else if (warp < TM::kWarpEpi + 4) {
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lanes 32q..32q+31
     const uint32_t dempty_leader = mapa_shared(s.dempty, 0);
@@ -480,7 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
       HB(10, ui);
       // woken by the polling warp once dfull[acc] has completed (a hardware
       // barrier: no issue slots burnt while the unit is computed)
-      named_bar_sync(kBarEpi + acc, 5 * 32);
+      named_bar_sync(TM::kBarEpi + acc, 5 * 32);
       HB(11, ui);
       tc_fence_after();
       const int rb = 2 * un.rp + static_cast<int>(rank);
@@ -515,7 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(dempty_leader + 8 * acc);
     }
-  } else if (warp == kWarpStream) {
+  } else if (warp == TM::kWarpStream) {
     // ---------------------------------------------------------------- entry stream
     // The CTA's entry stream is the concatenation of its units' entry ranges
     // [offsets[first tile], offsets[last tile + 1]) (contiguous per unit: tiles are
@@ -585,7 +591,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
         }
       }
     }
-  } else if (warp == kWarpX) {
+  } else if (warp == TM::kWarpX) {
     // ---------------------------------------------------------------- X stages
     // TMA loads of this CTA's half of the B columns, kTX k-tiles per stage; both
     // halves complete on the even CTA's xfull barrier (.cta_group::2). A TMA
@@ -609,7 +615,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
         }
       }
     }
-  } else if (warp == kWarpPoll) {
+  } else if (warp == TM::kWarpPoll) {
     // ---------------------------------------------------------------- polling warp
     // Non-blocking checks only (mbarrier.test_wait), no TMA issue: (a) per-tile
     // metadata (stream offset, groups), 32 tiles per step, one lane per tile,
@@ -642,19 +648,19 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
     while (gt < ntiles || eu < nunits || rel < ntiles) {
       bool progress = false;
       // (d) buffer releases: the MMA of tile rel committed -> wake the team that
-      //     decodes tile rel + kNA into the same buffer
-      //     (commits come per group of kG buffers: rel is a multiple of kG)
+      //     decodes tile rel + TM::kNA into the same buffer
+      //     (commits come per group of TM::kG buffers: rel is a multiple of TM::kG)
       while (rel < ntiles &&
-             __shfl_sync(0xffffffffu, mbar_test_wait(s.aempty + 8 * ((rel % kNA) / kG), (rel / kNA) & 1) ? 1 : 0, 0)) {
-        if (lane == 0) TRACE(15, rel / kG);
-        for (uint32_t t = rel; t < rel + kG && t + kNA < ntiles; ++t)
-          asm volatile("bar.arrive %0, %1;" ::"r"(kBarBuf + (t % kNA)), "r"((kTeamWarps + 1) * 32) : "memory");
-        rel += kG;
+             __shfl_sync(0xffffffffu, mbar_test_wait(s.aempty + 8 * ((rel % TM::kNA) / TM::kG), (rel / TM::kNA) & 1) ? 1 : 0, 0)) {
+        if (lane == 0) TRACE(15, rel / TM::kG);
+        for (uint32_t t = rel; t < rel + TM::kG && t + TM::kNA < ntiles; ++t)
+          asm volatile("bar.arrive %0, %1;" ::"r"(1 + (t % TM::kNA)), "r"((TM::kTeamWarps + 1) * 32) : "memory");
+        rel += TM::kG;
         progress = true;
       }
       // (c) epilogue wake-ups (the whole warp arrives on the named barrier)
       while (eu < nunits && __shfl_sync(0xffffffffu, mbar_test_wait(s.dfull + 8 * (eu & 1), (eu >> 1) & 1) ? 1 : 0, 0)) {
-        asm volatile("bar.arrive %0, %1;" ::"r"(kBarEpi + (eu & 1)), "r"(5 * 32) : "memory");
+        asm volatile("bar.arrive %0, %1;" ::"r"(TM::kBarEpi + (eu & 1)), "r"(5 * 32) : "memory");
         ++eu;
         progress = true;
       }
@@ -700,7 +706,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
         if (clock64() - idle_t0 > 40000000000LL) __trap();  // watchdog, as in mbar_wait
       }
     }
-  } else if (warp == kWarpMma && rank == 0) {
+  } else if (warp == TM::kWarpMma && rank == 0) {
     // ---------------------------------------------------------------- MMA issuer (even CTA)
     // The whole warp walks the schedule; one elected lane issues.
     const uint64_t a_desc0 = smem_desc(s.a, 128, 1024, 0);
@@ -723,9 +729,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
         HB(40, gt);
         if (lane == 0) TRACE(8, gt);
         if (in_stage == 0) mbar_wait_cluster(s.xfull + 8 * xs, (gs / NX) & 1);
-        const uint32_t b = gt % kNA;
+        const uint32_t b = gt % TM::kNA;
         if (lane == 0) TRACE(3, gt);
-        if (gt % kG == 0) mbar_wait_cluster(s.afull + 8 * (b / kG), (gt / kNA) & 1);  // all tiles of the group
+        if (gt % TM::kG == 0) mbar_wait_cluster(s.afull + 8 * (b / TM::kG), (gt / TM::kNA) & 1);  // all tiles of the group
         if (lane == 0) TRACE(4, gt);
         tc_fence_after();
         const uint64_t ad = a_desc0 + ((b * kABytes) >> 4);
@@ -737,7 +743,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
             if (!DBG(2))
               mma_f16_ss_pair(d_tmem, ad + (k4 * 256 >> 4), bd + (k4 * C::kKStep >> 4), C::kIdesc,
                               (kt > un.kt0 || k4 > 0) ? 1u : 0u);
-          if (gt % kG == kG - 1 || gt + 1 == total) mma_commit_pair(s.aempty + 8 * (b / kG), 3);
+          if (gt % TM::kG == TM::kG - 1 || gt + 1 == total) mma_commit_pair(s.aempty + 8 * (b / TM::kG), 3);
           TRACE(7, gt);
           if (stage_done) mma_commit_pair(s.xempty + 8 * xs, 3);
         }
@@ -754,7 +760,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(72)
   tc_fence_before();
   cluster_sync_all();
   HB(51, 0);
-  if (warp == kWarpMma) {
+  if (warp == TM::kWarpMma) {
     tc_fence_after();
     tmem_dealloc_pair(tmem, C::kTmemCols);
   }
@@ -781,16 +787,16 @@ int half_n(int n) {
   return 128;
 }
 
-template <int NH>
+template <int NH, class TM>
 int max_clusters() {
   static int cached = 0;
   if (!cached) {
-    using C = Cfg<NH>;
-    cudaFuncSetAttribute(spmm_sm100_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    using C = Cfg<NH, TM::kNA>;
+    cudaFuncSetAttribute(spmm_sm100_kernel<NH, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(C::kSmem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * 74, 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.blockDim = dim3(TM::kThreads, 1, 1);
     cfg.dynamicSmemBytes = C::kSmem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -800,7 +806,7 @@ int max_clusters() {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nc = 0;
-    if (cudaOccupancyMaxActiveClusters(&nc, spmm_sm100_kernel<NH>, &cfg) != cudaSuccess || nc <= 0) {
+    if (cudaOccupancyMaxActiveClusters(&nc, spmm_sm100_kernel<NH, TM>, &cfg) != cudaSuccess || nc <= 0) {
       cudaGetLastError();
       nc = num_sms() / 2;
     }
@@ -827,14 +833,28 @@ double split_cost(int tiles_mp, int tiles_k, int split, int clusters, double t_t
   return worst;
 }
 
+template <int NH, class TM>
+cudaError_t launch_shape(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
+  using C = Cfg<NH, TM::kNA>;
+  static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
+  const int nc = std::min(clusters, max_clusters<NH, TM>());
+  if ((p.units + nc - 1) / nc > kMaxUnits) return cudaErrorInvalidConfiguration;  // unit table size
+  spmm_sm100_kernel<NH, TM><<<2 * nc, TM::kThreads, C::kSmem, s>>>(tm, p);
+  return cudaGetLastError();
+}
+
+// Team shape for a matrix: 2-warp teams while a warp's share of a mean tile
+// (mean groups / 2) leaves headroom under kGMax, else 4-warp teams.
+bool sparse_teams(uint64_t n_entries, uint64_t tiles) {
+  const double mean_groups = tiles ? static_cast<double>(n_entries) / 32.0 / static_cast<double>(tiles) : 0.0;
+  return mean_groups <= 0.8 * kGMax * TeamsSparse::kTeamWarps;
+}
+
 template <int NH>
 cudaError_t launch_nh(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
-  using C = Cfg<NH>;
-  static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
-  const int nc = std::min(clusters, max_clusters<NH>());
-  if ((p.units + nc - 1) / nc > kMaxUnits) return cudaErrorInvalidConfiguration;  // unit table size
-  spmm_sm100_kernel<NH><<<2 * nc, kThreads, C::kSmem, s>>>(tm, p);
-  return cudaGetLastError();
+  const uint64_t tiles = static_cast<uint64_t>(p.tiles_m) * p.tiles_k;
+  if (sparse_teams(p.n_entries, tiles)) return launch_shape<NH, TeamsSparse>(p, tm, clusters, s);
+  return launch_shape<NH, TeamsDense>(p, tm, clusters, s);
 }
 
 }  // namespace
