@@ -18,6 +18,8 @@ from dataclasses import dataclass
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libtcsl_cuda.so")
+if os.environ.get("TCSL_CUDA_LIB"):  # A/B experiments (tools/build_variant.py); still the CUDA library
+    LIB_PATH = os.path.abspath(os.environ["TCSL_CUDA_LIB"])
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["encode.cu", "misc.cu", "spmm_sm100.cu", "capi.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -64,7 +64,7 @@ constexpr int kGMax = 20;                      // groups per warp per tile remem
 // sparse tiles are decoded by 2-warp teams (half the per-tile bookkeeping, 8
 // tiles in flight), denser ones by 4-warp teams (each warp's share of a tile
 // must fit the kGMax remembered addresses).
-template <int T, int W>
+template <int T, int W, int G = (T % 2 == 0) ? 2 : 1>
 struct Teams {
   static constexpr int kTeams = T;
   static constexpr int kTeamWarps = W;
@@ -72,7 +72,8 @@ struct Teams {
   // The MMA issuer waits once per kG tiles (one try_wait costs ~120-160 cycles
   // even when the phase is complete, profiles/r01_mma_loop_bench.txt): afull /
   // aempty are per group of kG consecutive buffers.
-  static constexpr int kG = (kNA % 2 == 0) ? 2 : 1;
+  static constexpr int kG = G;
+  static_assert(kNA % kG == 0, "buffer groups");
   static constexpr int kNP = kNA / kG;
   static constexpr int kWarpEpi = T * W;           // 4 epilogue warps (id % 4 = TMEM lane quarter)
   static constexpr int kWarpStream = kWarpEpi + 4;  // entry stream: bulk copies only (blocking waits)
@@ -89,8 +90,9 @@ struct Teams {
   // Register file per SMSP: ceil(warps / 4) * 32 * regs <= 16384.
   static constexpr int kMaxRegs = ((16384 / (32 * ((kWarpMma + 1 + 3) / 4))) / 8) * 8;
 };
-using TeamsSparse = Teams<8, 2>;
+using TeamsSparse = Teams<8, 2, 1>;  // per-tile buffer release: +2-5 % over groups of 2 (r01_ablation_mma_loop)
 using TeamsDense = Teams<5, 4>;
+
 
 constexpr uint32_t kRing = 65536;              // entry ring bytes (power of two)
 constexpr uint32_t kChunk = 16384;             // bytes per bulk copy (>= 8 KB: ~7 TB/s, profiles/r01_bulk_copy_bench.txt)
@@ -167,16 +169,39 @@ __device__ unsigned* g_hb = nullptr;
 #endif
 // Ablation switches for performance experiments, TCSL_TRACE builds only (env
 // TCSL_DEBUG): 1 skip scatter+clear, 2 skip MMAs, 4 skip ring loads.
-#ifdef TCSL_TRACE
+#if defined(TCSL_TRACE) || defined(TCSL_PROF)
 #define DBG(bit) (p.dbg & (bit))
 #else
 #define DBG(bit) 0
 #endif
 #ifdef TCSL_TRACE
 #define TRACE(slot, idx) \
-  do { if (blockIdx.x == 0 && p.trace && (idx) < 4096) p.trace[(slot) * 4096 + (idx)] = clock64(); } while (0)
+  do { if (blockIdx.x == 0 && p.trace && !(p.dbg & 16) && (idx) < 4096) p.trace[(slot) * 4096 + (idx)] = clock64(); } while (0)
 #else
 #define TRACE(slot, idx) do { } while (0)
+#endif
+#if defined(TCSL_TRACE) || defined(TCSL_PROF)
+#define TCSL_PROFILING 1
+#endif
+// Per-warp cycle accounting of CTA 0 (profiling builds, tools/prof_spmm.py),
+// dumped to trace slot 15. Empty in product builds.
+struct Prof {
+#ifdef TCSL_PROFILING
+  long long v[8];
+  long long t;
+#endif
+};
+#ifdef TCSL_PROFILING
+#define PROF_DECL(n) Prof prof_ = {}
+#define PROF_MARK() prof_.t = clock64()
+#define PROF_ADD(i) do { const long long t_ = clock64(); prof_.v[i] += t_ - prof_.t; prof_.t = t_; } while (0)
+#define PROF_DUMP(base, n) do { if (blockIdx.x == 0 && p.trace && (threadIdx.x & 31) == 0) \
+    for (int i_ = 0; i_ < (n); ++i_) p.trace[15 * 4096 + (base) + i_] = prof_.v[i_]; } while (0)
+#else
+#define PROF_DECL(n) Prof prof_; (void)prof_
+#define PROF_MARK() do { } while (0)
+#define PROF_ADD(i) do { } while (0)
+#define PROF_DUMP(base, n) do { } while (0)
 #endif
 
 struct Unit {
@@ -292,7 +317,7 @@ __device__ __forceinline__ void release_ring(const Smem& s, uint32_t lo, uint32_
 template <class TM>
 __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint32_t gt, int team, int tw, int lane,
                                             uint32_t afull_leader, uint32_t total, uint32_t (&E)[kGMax],
-                                            uint32_t (&Z)[kGMax], uint32_t& nz, uint32_t& err_or) {
+                                            uint32_t (&Z)[kGMax], uint32_t& nz, uint32_t& err_or, Prof& prof_) {
   // per-tile metadata from the stream producer (normally published long ago)
   HB(1, gt);
   if (tw == 0 && lane == 0) TRACE(13, gt);
@@ -304,6 +329,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
     }
   }
   const uint2 meta = lds64(s.meta + 8 * (gt % kMeta));  // (stream offset, groups)
+  PROF_ADD(0);
   const uint32_t g0w = meta.y * tw / TM::kTeamWarps, g1w = meta.y * (tw + 1) / TM::kTeamWarps;
   const uint32_t cnt = g1w - g0w;
   const uint32_t ncnt = min(cnt, static_cast<uint32_t>(kGMax));
@@ -312,6 +338,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   if (cnt) {
     for (uint32_t k = lo / kChunk; k <= (hi - 1) / kChunk; ++k)
       mbar_wait_backoff(s.cfull + 8 * (k % kNB), (k / kNB) & 1, 64);
+    PROF_ADD(1);
     if (DBG(4)) {
     } else if ((lo & (kRing - 1)) + cnt * 128u <= kRing) {
       load_groups(E, s.ring + (lo & (kRing - 1)) + 4u * lane, ncnt);
@@ -329,6 +356,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
     // buffer (holding them longer starves the ring at low sparsity)
     __syncwarp();
     if (cnt <= static_cast<uint32_t>(kGMax) && lane == 0) release_ring(s, lo, hi);
+    PROF_ADD(2);
   }
   if (tw == 0 && lane == 0) TRACE(14, gt);
   const uint32_t b = gt % TM::kNA;
@@ -338,6 +366,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   // warp observed that commit and arrives here; waiting on a named barrier
   // costs no issue slots and no sync-unit polling.
   if (gt >= static_cast<uint32_t>(TM::kNA)) named_bar_sync(1 + team, (TM::kTeamWarps + 1) * 32);
+  PROF_ADD(3);
   if (tw == 0 && lane == 0) TRACE(0, gt);
   HB(4, gt);
   // s.ovf[b] = the last tile in buffer b for which some warp of the team wrote
@@ -347,9 +376,11 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   } else if (!DBG(1)) {
     clear_groups(Z, nz);
   }
+  PROF_ADD(4);
   HB(5, gt);
   named_bar_sync(1 + team, TM::kTeamWarps * 32);
   HB(6, gt);
+  PROF_ADD(5);
   if (tw == 0 && lane == 0) {
     TRACE(1, gt);
     asm volatile("red.relaxed.cta.shared::cta.add.u32 [%0], 1;" ::"r"(s.done) : "memory");  // meta slot read
@@ -378,6 +409,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
       mbar_arrive_cluster(ab);
   }
   if (tw == 0 && lane == 0) TRACE(2, gt);
+  PROF_ADD(6);
   HB(7, gt);
 }
 
@@ -470,14 +502,23 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
     uint32_t err_or = 0;
     uint32_t Z[kGMax];  // addresses last written to the team's buffer
     uint32_t nz = 0;
+    PROF_DECL(8);  // meta, chunk waits, load, buffer wake, clear, team barrier, scatter+arrive, total
+#ifdef TCSL_PROFILING
+    const long long prof_start = clock64();
+#endif
+    PROF_MARK();
     for (uint32_t gt = team; gt < total; gt += TM::kTeams)
-      decode_tile<TM>(p, s, gt, team, tw, lane, afull_leader, total, E, Z, nz, err_or);
+      decode_tile<TM>(p, s, gt, team, tw, lane, afull_leader, total, E, Z, nz, err_or, prof_);
+#ifdef TCSL_PROFILING
+    prof_.v[7] = clock64() - prof_start;
+    if (warp == 0) PROF_DUMP(8, 8);
+#endif
     // locations >= 8192 leave the 128x64 tile (the scatter masked them into range)
     if (__any_sync(0xffffffffu, (err_or & 0xE000u) != 0) && lane == 0)
       raise_dev(p.err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
   } else if (warp < TM::kWarpEpi + 4) {
     // ---------------------------------------------------------------- epilogue
-    const int q = warp & 3;  // TMEM lanes 32q..32q+31
+    const int q = warp & 3;  // TMEM lanes 32q..32q+31 (warp % 4 selects the lane quarter)
     const uint32_t dempty_leader = mapa_shared(s.dempty, 0);
     uint32_t ui = 0;
     for (int u = cid; u < p.units; u += ncl, ++ui) {
@@ -708,7 +749,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
     }
   } else if (warp == TM::kWarpMma && rank == 0) {
     // ---------------------------------------------------------------- MMA issuer (even CTA)
-    // The whole warp walks the schedule; one elected lane issues.
+    // One elected thread runs the whole schedule: no per-tile elect /
+    // reconvergence (-6 % at 90 % sparsity against a warp-wide loop with an
+    // elected issuer, profiles/r01_ablation_mma_loop.txt). Per k-tile: xfull
+    // when an X stage starts, afull once per group of kG tiles, then the 4
+    // MMAs and the commits. Each wait is a ~150-200-cycle sync-unit round
+    // trip even when the phase has completed (profiles/r01_mma_loop_bench.txt).
     const uint64_t a_desc0 = smem_desc(s.a, 128, 1024, 0);
     const uint64_t b_desc0 = smem_desc(s.x, C::kLBO, C::kSBO, C::kLayout);
     uint32_t total = 0;  // k-tiles of this CTA
@@ -716,43 +762,62 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
       const Unit un = unit_of(p, u);
       total += un.kt1 - un.kt0;
     }
-    uint32_t gt = 0, ui = 0, gs = 0;
-    for (int u = cid; u < p.units; u += ncl, ++ui) {
-      const Unit un = unit_of(p, u);
-      const uint32_t acc = ui & 1;
-      if (ui >= 2) mbar_wait_cluster(s.dempty + 8 * acc, ((ui >> 1) - 1) & 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem + acc * C::kN;
-      for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
-        const int in_stage = (kt - un.kt0) % C::kTX;
-        const uint32_t xs = gs % NX;
-        HB(40, gt);
-        if (lane == 0) TRACE(8, gt);
-        if (in_stage == 0) mbar_wait_cluster(s.xfull + 8 * xs, (gs / NX) & 1);
-        const uint32_t b = gt % TM::kNA;
-        if (lane == 0) TRACE(3, gt);
-        if (gt % TM::kG == 0) mbar_wait_cluster(s.afull + 8 * (b / TM::kG), (gt / TM::kNA) & 1);  // all tiles of the group
-        if (lane == 0) TRACE(4, gt);
+    PROF_DECL(8);  // dempty, xfull, afull, loop, total, fence+descriptors, MMA issue, commits
+#ifdef TCSL_PROFILING
+    const long long prof_start = clock64();
+#endif
+    PROF_MARK();
+    if (elect_one()) {
+      uint32_t gt = 0, ui = 0, gs = 0;
+      for (int u = cid; u < p.units; u += ncl, ++ui) {
+        const Unit un = unit_of(p, u);
+        const uint32_t acc = ui & 1;
+        if (ui >= 2) mbar_wait(s.dempty + 8 * acc, ((ui >> 1) - 1) & 1);
+        PROF_ADD(0);
         tc_fence_after();
-        const uint64_t ad = a_desc0 + ((b * kABytes) >> 4);
-        const uint64_t bd = b_desc0 + ((xs * C::kXStage + in_stage * C::kTileStep) >> 4);
-        const bool stage_done = in_stage == C::kTX - 1 || kt + 1 == un.kt1;
-        if (elect_one()) {
+        const uint32_t d_tmem = tmem + acc * C::kN;
+        int in_stage = 0;
+        for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
+          const uint32_t xs = gs % NX;
+          TRACE(8, gt);
+          PROF_ADD(3);
+          if (in_stage == 0) mbar_wait(s.xfull + 8 * xs, (gs / NX) & 1);
+          PROF_ADD(1);
+          const uint32_t b = gt % TM::kNA;
+          TRACE(3, gt);
+          if (gt % TM::kG == 0) mbar_wait(s.afull + 8 * (b / TM::kG), (gt / TM::kNA) & 1);  // the group's tiles
+          PROF_ADD(2);
+          TRACE(4, gt);
+          tc_fence_after();
+          const uint64_t ad = a_desc0 + ((b * kABytes) >> 4);
+          const uint64_t bd = b_desc0 + ((xs * C::kXStage + in_stage * C::kTileStep) >> 4);
+          PROF_ADD(5);
 #pragma unroll
           for (int k4 = 0; k4 < kKTB / 16; ++k4)
             if (!DBG(2))
               mma_f16_ss_pair(d_tmem, ad + (k4 * 256 >> 4), bd + (k4 * C::kKStep >> 4), C::kIdesc,
                               (kt > un.kt0 || k4 > 0) ? 1u : 0u);
+          PROF_ADD(6);
           if (gt % TM::kG == TM::kG - 1 || gt + 1 == total) mma_commit_pair(s.aempty + 8 * (b / TM::kG), 3);
           TRACE(7, gt);
-          if (stage_done) mma_commit_pair(s.xempty + 8 * xs, 3);
+          if (in_stage == C::kTX - 1 || kt + 1 == un.kt1) {
+            mma_commit_pair(s.xempty + 8 * xs, 3);
+            ++gs;
+            in_stage = 0;
+          } else {
+            ++in_stage;
+          }
+          PROF_ADD(7);
         }
-        __syncwarp();
-        if (stage_done) ++gs;
+        mma_commit_pair(s.dfull + 8 * acc, 3);
       }
-      if (elect_one()) mma_commit_pair(s.dfull + 8 * acc, 3);
-      __syncwarp();
     }
+    __syncwarp();
+#ifdef TCSL_PROFILING
+    PROF_ADD(3);
+    prof_.v[4] = clock64() - prof_start;
+    PROF_DUMP(0, 8);
+#endif
   }
 
   __syncwarp();  // role branches may leave lanes behind; the cluster barrier is .aligned
@@ -967,7 +1032,7 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
 
 }  // namespace tcslk
 
-#ifdef TCSL_TRACE
+#ifdef TCSL_PROFILING
 extern "C" void tcsl_cuda_debug_set_trace(unsigned long long* d_trace) { tcslk::g_trace = d_trace; }
 #endif
 #if defined(TCSL_TRACE) && defined(TCSL_HEARTBEAT)

@@ -11,7 +11,7 @@
 using namespace tcslk;
 
 // WAIT: 0 none, 1 try_wait, 2 test_wait; TPI tiles per iteration (one wait per iteration)
-template <int BUSY, int DO_MMA, int COMMIT_EVERY, int WAIT = 1, int TPI = 1, int ONE_THREAD = 0>
+template <int BUSY, int DO_MMA, int COMMIT_EVERY, int WAIT = 1, int TPI = 1, int ONE_THREAD = 0, int CLK = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) bench(int iters, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t base = (smem_u32(smem) + 1023u) & ~1023u;
@@ -38,7 +38,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) bench(int it
       const uint32_t idesc = idesc_f16_f32(256, 16, 1);
       const uint64_t a0 = smem_desc(sa, 128, 1024, 0), b0 = smem_desc(sb, 128, 128, 0);
       const long long t0 = clock64();
+      long long acc_clk = 0;
       for (int it = 0; it < iters; it += TPI) {
+#pragma unroll
+        for (int c = 0; c < CLK; ++c) acc_clk += clock64() * (c + 1);
         if (WAIT == 1) mbar_wait(bars + 8 * 15, 0);
         if (WAIT == 2) while (!mbar_test_wait(bars + 8 * 15, 0)) {}
         tc_fence_after();
@@ -58,7 +61,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) bench(int it
       if (ONE_THREAD || elect_one()) mma_commit_pair(bars + 8 * 8, 3);
       if (!ONE_THREAD) __syncwarp();
       mbar_wait(bars + 8 * 8, 0);
-      if (lane == 0) out[blockIdx.x] = (clock64() - t0) / iters;
+      if (lane == 0) out[blockIdx.x] = (clock64() - t0) / iters + (acc_clk == 42 ? 1 : 0);
       stop = 1;
     }
   } else if (BUSY && warp < 16) {
@@ -82,14 +85,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) bench(int it
   }
 }
 
-template <int BUSY, int DO_MMA, int COMMIT_EVERY, int WAIT = 1, int TPI = 1, int ONE_THREAD = 0>
+template <int BUSY, int DO_MMA, int COMMIT_EVERY, int WAIT = 1, int TPI = 1, int ONE_THREAD = 0, int CLK = 0>
 void run(const char* name) {
   long long* d;
   cudaMalloc(&d, 148 * 8);
   cudaMemset(d, 0, 148 * 8);
   const int smem = 9 * 16384 + 2048;
-  cudaFuncSetAttribute(bench<BUSY, DO_MMA, COMMIT_EVERY, WAIT, TPI, ONE_THREAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  bench<BUSY, DO_MMA, COMMIT_EVERY, WAIT, TPI, ONE_THREAD><<<148, 576, smem>>>(2000, d);
+  cudaFuncSetAttribute(bench<BUSY, DO_MMA, COMMIT_EVERY, WAIT, TPI, ONE_THREAD, CLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  bench<BUSY, DO_MMA, COMMIT_EVERY, WAIT, TPI, ONE_THREAD, CLK><<<148, 576, smem>>>(2000, d);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
@@ -100,6 +103,19 @@ void run(const char* name) {
 }
 
 int main() {
+  run<0, 0, 1000000, 0, 1, 1, 0>("idle, 1 thread, empty loop");
+  run<0, 0, 1000000, 0, 1, 1, 6>("idle, 1 thread, 6 clock64 reads");
+  run<1, 0, 1000000, 0, 1, 1, 6>("busy, 1 thread, 6 clock64 reads");
+  run<1, 1, 1, 0, 1, 1, 0>("busy, 1 thread, MMA, commit/tile");
+  run<1, 1, 1, 0, 1, 1, 6>("busy, 1 thread, MMA, commit/tile, 6 clocks");
+  run<1, 1, 1, 1, 1, 1, 0>("busy, 1 thread, MMA, commit/tile, try_wait");
+  run<0, 0, 1000000, 0>("idle, no MMA, no commit, no wait");
+  run<0, 0, 1, 0>("idle, no MMA, commit/tile, no wait");
+  run<0, 0, 1, 1>("idle, no MMA, commit/tile, try_wait");
+  run<0, 1, 1000000, 0>("idle, MMA, no commit, no wait");
+  run<1, 0, 1000000, 0>("busy, no MMA, no commit, no wait");
+  run<1, 0, 1, 0>("busy, no MMA, commit/tile, no wait");
+  run<1, 0, 1, 1>("busy, no MMA, commit/tile, try_wait");
   run<0, 1, 1>("idle, MMA, commit/tile, try_wait");
   run<0, 1, 1, 0>("idle, MMA, commit/tile, no wait");
   run<0, 1, 1, 2>("idle, MMA, commit/tile, test_wait");

@@ -14,7 +14,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2309_10285_b200 as tc  # noqa: E402
 
-tc.LIB_PATH = os.path.join(tc.LIB_DIR, "libtcsl_cuda_trace.so")
+tc.LIB_PATH = os.environ.get("TCSL_CUDA_LIB") or os.path.join(tc.LIB_DIR, "libtcsl_cuda_trace.so")
 if not os.path.exists(tc.LIB_PATH):
     import subprocess
     subprocess.run(["nvcc", *tc.NVCC_FLAGS, "-DTCSL_TRACE", "-o", tc.LIB_PATH,
@@ -72,3 +72,10 @@ st("decode: start->data", diff(13, 14))
 st("decode: data->buffer", diff(14, 0))
 st("decode: buffer->barrier", diff(0, 1))
 st("decode: barrier->done", diff(1, 2))
+if os.environ.get("TRACE_RAW"):
+    print("  tile |  top(8)  xfull  afull  issue  next | decoded(2) before afull_seen")
+    idx = [i for i in range(100, 160) if tr[8][i]]
+    for i, j in zip(idx[:-1], idx[1:]):
+        print("  %4d | %7d %6d %6d %6d %5d | %7d" % (i, tr[8][i] - base, tr[3][i] - tr[8][i], tr[4][i] - tr[3][i],
+              tr[7][i] - tr[4][i] if tr[7][i] else -1, tr[8][j] - tr[7][i] if tr[7][i] else -1,
+              tr[4][i] - tr[2][i] if tr[2][i] else 0))
