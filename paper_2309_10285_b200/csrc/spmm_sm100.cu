@@ -90,13 +90,25 @@ struct Teams {
   // Register file per SMSP: ceil(warps / 4) * 32 * regs <= 16384.
   static constexpr int kMaxRegs = ((16384 / (32 * ((kWarpMma + 1 + 3) / 4))) / 8) * 8;
 };
-using TeamsSparse = Teams<8, 2, 1>;  // per-tile buffer release: +2-5 % over groups of 2 (r01_ablation_mma_loop)
+#ifndef TCSL_SPARSE_G
+#define TCSL_SPARSE_G 1
+#endif
+#ifndef TCSL_QUAD
+#define TCSL_QUAD 1
+#endif
+constexpr bool kQuad = TCSL_QUAD;  // issue a whole 4-tile X stage per MMA-loop iteration
+using TeamsSparse = Teams<8, 2, TCSL_SPARSE_G>;  // G=1, per-tile release: +2-5 % over G=2 (r01_ablation_mma_loop)
 using TeamsDense = Teams<5, 4>;
+#ifndef TCSL_SPARSE9
+#define TCSL_SPARSE9 0
+#endif
+// N <= 16 leaves room for a ninth buffer (X stages take 16 KB instead of 32 KB)
+using TeamsSparse9 = Teams<9, 2, 1>;
 
 
-constexpr uint32_t kRing = 65536;              // entry ring bytes (power of two)
+constexpr uint32_t kRingMin = 65536;           // entry ring bytes (power of two; Cfg::kRing may be larger)
 constexpr uint32_t kChunk = 16384;             // bytes per bulk copy (>= 8 KB: ~7 TB/s, profiles/r01_bulk_copy_bench.txt)
-constexpr int kNR = kRing / kChunk;            // chunks in flight
+constexpr int kNRMax = 8;                      // cempty barriers reserved (ring <= 128 KB)
 // "chunk landed" barriers: chunk k uses cfull[k % kNB]. A decoder may wait for a
 // chunk up to ~9 tiles (<= 45 chunks) past the oldest unconsumed one; with more
 // barriers than that, the barrier's previous phase is always complete, so the
@@ -131,6 +143,10 @@ struct Cfg {
   // start on sm_100: the driver reserves the first 1 KB): entry ring, small
   // tables, X stages, then the dense-tile buffers at the next 16 KB-aligned
   // address (so a tile address is base | offset, one LOP3 in the scatter).
+  // Entry ring: 64 KB (a 128 KB ring where it fits, dense tiles at N <= 16,
+  // measured neutral).
+  static constexpr uint32_t kRing = kRingMin;
+  static constexpr int kNR = kRing / kChunk;
   static constexpr uint32_t kOffRing = 0;
   static constexpr uint32_t kOffSmall = kRing;
   static constexpr uint32_t kOffX = kOffSmall + kSmallBytes;  // 1 KB aligned
@@ -305,16 +321,17 @@ struct Smem {
 
 // Count a warp's consumed stream bytes [lo, hi) on the chunks' "consumed"
 // barriers (the stream warp refills a chunk once all of its bytes are consumed).
+template <int NR>
 __device__ __forceinline__ void release_ring(const Smem& s, uint32_t lo, uint32_t hi) {
   for (uint32_t k = lo / kChunk; k <= (hi - 1) / kChunk; ++k) {
     const uint32_t c0 = max(lo, k * kChunk), c1 = min(hi, (k + 1) * kChunk);
-    mbar_complete_tx(s.cempty + 8 * (k % kNR), c1 - c0);
+    mbar_complete_tx(s.cempty + 8 * (k % NR), c1 - c0);
   }
 }
 
 // One decode warp's part of tile gt (see the file comment). Z / nz describe
 // what this warp last wrote into the tile's buffer.
-template <class TM>
+template <class TM, uint32_t RING>
 __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint32_t gt, int team, int tw, int lane,
                                             uint32_t afull_leader, uint32_t total, uint32_t (&E)[kGMax],
                                             uint32_t (&Z)[kGMax], uint32_t& nz, uint32_t& err_or, Prof& prof_) {
@@ -340,12 +357,12 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
       mbar_wait_backoff(s.cfull + 8 * (k % kNB), (k / kNB) & 1, 64);
     PROF_ADD(1);
     if (DBG(4)) {
-    } else if ((lo & (kRing - 1)) + cnt * 128u <= kRing) {
-      load_groups(E, s.ring + (lo & (kRing - 1)) + 4u * lane, ncnt);
+    } else if ((lo & (RING - 1)) + cnt * 128u <= RING) {
+      load_groups(E, s.ring + (lo & (RING - 1)) + 4u * lane, ncnt);
     } else {  // this warp's span wraps around the ring end
 #pragma unroll
       for (int j = 0; j < kGMax; ++j)
-        if (static_cast<uint32_t>(j) < ncnt) E[j] = lds32(s.ring + ((lo + j * 128u) & (kRing - 1)) + 4u * lane);
+        if (static_cast<uint32_t>(j) < ncnt) E[j] = lds32(s.ring + ((lo + j * 128u) & (RING - 1)) + 4u * lane);
     }
     // locations must stay inside the 128x64 tile; slots past ncnt hold this
     // warp's earlier (already checked) entries
@@ -355,7 +372,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
     // bytes back at once so the stream refills while this tile waits for its
     // buffer (holding them longer starves the ring at low sparsity)
     __syncwarp();
-    if (cnt <= static_cast<uint32_t>(kGMax) && lane == 0) release_ring(s, lo, hi);
+    if (cnt <= static_cast<uint32_t>(kGMax) && lane == 0) release_ring<RING / kChunk>(s, lo, hi);
     PROF_ADD(2);
   }
   if (tw == 0 && lane == 0) TRACE(14, gt);
@@ -389,13 +406,13 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   nz = DBG(1) ? 0 : ncnt;
   if (cnt > static_cast<uint32_t>(kGMax)) {  // dense tiles (> ~25 % nonzeros)
     for (uint32_t g = kGMax; g < cnt; ++g) {
-      const uint32_t e = lds32(s.ring + ((lo + g * 128u) & (kRing - 1)) + 4u * lane);
+      const uint32_t e = lds32(s.ring + ((lo + g * 128u) & (RING - 1)) + 4u * lane);
       err_or |= e;
       sts16(a_addr(a_tile, e), e >> 16);
     }
     if (lane == 0) st_shared_u32(s.ovf + 4 * b, gt);
   }
-  if (cnt > static_cast<uint32_t>(kGMax) && lane == 0) release_ring(s, lo, hi);  // overflowed: read the ring until now
+  if (cnt > static_cast<uint32_t>(kGMax) && lane == 0) release_ring<RING / kChunk>(s, lo, hi);  // overflowed: read the ring until now
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
@@ -426,8 +443,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
   s.a = opaque(base + C::kOffA);
   const uint32_t sm = base + C::kOffSmall;
   s.cfull = opaque(sm);              // [kNB] ring chunk landed (bulk-copy bytes)
-  s.cempty = s.cfull + 8 * kNB;      // [kNR] ring chunk consumed (decoders' complete_tx bytes)
-  s.afull = s.cempty + 8 * kNR;      // [TM::kNP] even CTA: TM::kG tiles x 4 decode warps x 2 CTAs arrivals
+  s.cempty = s.cfull + 8 * kNB;      // [C::kNR] ring chunk consumed (decoders' complete_tx bytes)
+  s.afull = s.cempty + 8 * C::kNR;      // [TM::kNP] even CTA: TM::kG tiles x 4 decode warps x 2 CTAs arrivals
   s.aempty = s.afull + 8 * TM::kNP;      // [TM::kNP] both CTAs: MMA commit after the group's last tile
   s.xfull = s.aempty + 8 * TM::kNP;      // [NX] even CTA: 2 arrivals + both halves' bytes
   s.xempty = s.xfull + 8 * NX;       // [NX] both CTAs: MMA commit
@@ -442,7 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
   s.done = s.tiles_ready + 4;        // tiles whose metadata the decoders have read
   s.tab_ready = s.done + 4;          // unit table written (stream warp -> polling warp)
   s.tmem_slot = s.tab_ready + 4;
-  static_assert(8 * (kNB + kNR + 2 * TM::kNP + 2 * NX + 4 + kMeta) + 12 * kMaxUnits + 4 * TM::kNA + 16 <= kSmallBytes,
+  static_assert(8 * (kNB + C::kNR + 2 * TM::kNP + 2 * NX + 4 + kMeta) + 12 * kMaxUnits + 4 * TM::kNA + 16 <= kSmallBytes,
                 "small smem region");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (s.tmem_slot - base));
 
@@ -454,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNB; ++i) mbar_init(s.cfull + 8 * i, 1);
-    for (int i = 0; i < kNR; ++i) mbar_init(s.cempty + 8 * i, 1);
+    for (int i = 0; i < C::kNR; ++i) mbar_init(s.cempty + 8 * i, 1);
     for (int i = 0; i < TM::kNA; ++i) {
       if (i < TM::kNP) {
         mbar_init(s.afull + 8 * i, TM::kG * 2 * TM::kTeamWarps);
@@ -508,7 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
 #endif
     PROF_MARK();
     for (uint32_t gt = team; gt < total; gt += TM::kTeams)
-      decode_tile<TM>(p, s, gt, team, tw, lane, afull_leader, total, E, Z, nz, err_or, prof_);
+      decode_tile<TM, C::kRing>(p, s, gt, team, tw, lane, afull_leader, total, E, Z, nz, err_or, prof_);
 #ifdef TCSL_PROFILING
     prof_.v[7] = clock64() - prof_start;
     if (warp == 0) PROF_DUMP(8, 8);
@@ -567,9 +584,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
     // The CTA's entry stream is the concatenation of its units' entry ranges
     // [offsets[first tile], offsets[last tile + 1]) (contiguous per unit: tiles are
     // row-major over the tile grid, tcsl_format.cpp:56-57). Stream byte S lives at
-    // ring offset S % kRing and is fetched in kChunk-byte bulk copies (split at
+    // ring offset S % C::kRing and is fetched in kChunk-byte bulk copies (split at
     // unit boundaries); chunk k lands on cfull[k % kNB], decoders count consumed
-    // bytes on cempty[k % kNR] (complete_tx). A bulk-copy issue blocks for
+    // bytes on cempty[k % C::kNR] (complete_tx). A bulk-copy issue blocks for
     // hundreds of cycles under load, so this warp does nothing else.
     // 1. Validate every unit (monotone offsets, whole 32-entry groups, in range)
     //    into the unit table; an invalid unit streams no bytes and its tiles
@@ -612,8 +629,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
       bool have_unit = false;
       for (uint32_t k = 0; k < nchunks; ++k) {
         const uint32_t c0 = k * kChunk, c1 = min(total, c0 + kChunk);
-        if (k >= static_cast<uint32_t>(kNR)) mbar_wait(s.cempty + 8 * (k % kNR), ((k / kNR) - 1) & 1);
-        mbar_arrive_expect_tx(s.cempty + 8 * (k % kNR), c1 - c0);
+        if (k >= static_cast<uint32_t>(C::kNR)) mbar_wait(s.cempty + 8 * (k % C::kNR), ((k / C::kNR) - 1) & 1);
+        mbar_arrive_expect_tx(s.cempty + 8 * (k % C::kNR), c1 - c0);
         mbar_arrive_expect_tx(s.cfull + 8 * (k % kNB), c1 - c0);
         for (uint32_t pos = c0; pos < c1;) {
           if (!have_unit || pos >= ue) {
@@ -625,7 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
             continue;
           }
           const uint32_t pe = min(c1, ue);
-          bulk_g2s(s.ring + (pos & (kRing - 1)), p.ent + ug0 + (pos - us) / 4u, pe - pos, s.cfull + 8 * (k % kNB),
+          bulk_g2s(s.ring + (pos & (C::kRing - 1)), p.ent + ug0 + (pos - us) / 4u, pe - pos, s.cfull + 8 * (k % kNB),
                    pol);
           TRACE(6, k);
           pos = pe;
@@ -777,13 +794,21 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * C::kN;
         int in_stage = 0;
-        for (int kt = un.kt0; kt < un.kt1; ++kt, ++gt) {
+        for (int kt = un.kt0; kt < un.kt1;) {
           const uint32_t xs = gs % NX;
           TRACE(8, gt);
           PROF_ADD(3);
           if (in_stage == 0) mbar_wait(s.xfull + 8 * xs, (gs / NX) & 1);
           PROF_ADD(1);
           const uint32_t b = gt % TM::kNA;
+          // Several k-tiles per iteration when they share an X stage and sit
+          // in consecutive buffers (constant descriptor steps): a whole stage
+          // (kTX = 4 tiles) or a pair; the afull wait of each buffer group
+          // comes right before that group's MMAs.
+          const bool quad = kQuad && C::kTX == 4 && TM::kNA % 4 == 0 && (gt & 3) == 0 && in_stage == 0 &&
+                            kt + 3 < un.kt1;
+          const bool two = !quad && TM::kG == 2 && (gt & 1) == 0 && kt + 1 < un.kt1 && in_stage + 1 < C::kTX;
+          const uint32_t nt = quad ? 4u : (two ? 2u : 1u);
           TRACE(3, gt);
           if (gt % TM::kG == 0) mbar_wait(s.afull + 8 * (b / TM::kG), (gt / TM::kNA) & 1);  // the group's tiles
           PROF_ADD(2);
@@ -793,20 +818,34 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
           const uint64_t bd = b_desc0 + ((xs * C::kXStage + in_stage * C::kTileStep) >> 4);
           PROF_ADD(5);
 #pragma unroll
-          for (int k4 = 0; k4 < kKTB / 16; ++k4)
-            if (!DBG(2))
-              mma_f16_ss_pair(d_tmem, ad + (k4 * 256 >> 4), bd + (k4 * C::kKStep >> 4), C::kIdesc,
-                              (kt > un.kt0 || k4 > 0) ? 1u : 0u);
+          for (int j = 0; j < 4; ++j) {
+            if (j >= static_cast<int>(nt)) break;
+            if (j > 0 && (gt + j) % TM::kG == 0) {
+              mbar_wait(s.afull + 8 * ((b + j) / TM::kG), (gt / TM::kNA) & 1);
+              tc_fence_after();
+            }
+#pragma unroll
+            for (int k4 = 0; k4 < kKTB / 16; ++k4)
+              if (!DBG(2))
+                mma_f16_ss_pair(d_tmem, ad + ((j * kABytes + k4 * 256) >> 4),
+                                bd + ((j * C::kTileStep + k4 * C::kKStep) >> 4), C::kIdesc,
+                                (kt > un.kt0 || j > 0 || k4 > 0) ? 1u : 0u);
+            if (j + 1 < static_cast<int>(nt) && (gt + j) % TM::kG == TM::kG - 1)
+              mma_commit_pair(s.aempty + 8 * ((b + j) / TM::kG), 3);
+          }
           PROF_ADD(6);
-          if (gt % TM::kG == TM::kG - 1 || gt + 1 == total) mma_commit_pair(s.aempty + 8 * (b / TM::kG), 3);
+          const uint32_t last = gt + nt - 1;
+          if (last % TM::kG == TM::kG - 1 || last + 1 == total) mma_commit_pair(s.aempty + 8 * ((b + nt - 1) / TM::kG), 3);
           TRACE(7, gt);
-          if (in_stage == C::kTX - 1 || kt + 1 == un.kt1) {
+          if (in_stage + static_cast<int>(nt) == C::kTX || kt + static_cast<int>(nt) == un.kt1) {
             mma_commit_pair(s.xempty + 8 * xs, 3);
             ++gs;
             in_stage = 0;
           } else {
-            ++in_stage;
+            in_stage += nt;
           }
+          kt += nt;
+          gt += nt;
           PROF_ADD(7);
         }
         mma_commit_pair(s.dfull + 8 * acc, 3);
@@ -918,7 +957,10 @@ bool sparse_teams(uint64_t n_entries, uint64_t tiles) {
 template <int NH>
 cudaError_t launch_nh(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
   const uint64_t tiles = static_cast<uint64_t>(p.tiles_m) * p.tiles_k;
-  if (sparse_teams(p.n_entries, tiles)) return launch_shape<NH, TeamsSparse>(p, tm, clusters, s);
+  if (sparse_teams(p.n_entries, tiles)) {
+    if constexpr (TCSL_SPARSE9 && NH == 8) return launch_shape<NH, TeamsSparse9>(p, tm, clusters, s);
+    return launch_shape<NH, TeamsSparse>(p, tm, clusters, s);
+  }
   return launch_shape<NH, TeamsDense>(p, tm, clusters, s);
 }
 

@@ -79,3 +79,10 @@ if os.environ.get("TRACE_RAW"):
         print("  %4d | %7d %6d %6d %6d %5d | %7d" % (i, tr[8][i] - base, tr[3][i] - tr[8][i], tr[4][i] - tr[3][i],
               tr[7][i] - tr[4][i] if tr[7][i] else -1, tr[8][j] - tr[7][i] if tr[7][i] else -1,
               tr[4][i] - tr[2][i] if tr[2][i] else 0))
+if os.environ.get("TRACE_CHAIN"):
+    na = int(os.environ.get("TRACE_NA", "8"))
+    print("  tile | decoded  +mma_sees  +issued  +released  +woken(t+NA) | decode_start->done")
+    for i in range(100, 130):
+        print("  %4d | %7d %9d %8d %10d %12d | %7d" % (
+            i, tr[2][i] - base, tr[4][i] - tr[2][i], tr[7][i] - tr[4][i], tr[15][i] - tr[7][i],
+            tr[0][i + na] - tr[15][i] if tr[0][i + na] else -1, tr[2][i] - tr[13][i]))
