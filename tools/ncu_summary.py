@@ -16,6 +16,10 @@ KEYS = [
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "lts__t_sector_hit_rate.pct",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "launch__cluster_dim_x",
     "smsp__warps_active.avg.per_cycle_active",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg", "l1tex__data_pipe_tc_wavefronts_mem_shared.sum",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
 ]
 
 ap = argparse.ArgumentParser()
@@ -29,8 +33,9 @@ rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
 got = {}
 for h, u, v in zip(hdr, units, vals):
-    if h in KEYS:
-        got[h] = (v, u)
+    k = h.split(".", 2)[-1] if h.startswith(("TPC.", "SM_C.")) else h  # section-prefixed names
+    if k in KEYS:
+        got[k] = (v, u)
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 def nbytes(k):
     v, u = got.get(k, ("0", "byte"))
