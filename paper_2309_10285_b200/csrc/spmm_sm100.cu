@@ -114,7 +114,6 @@ using TeamsSparse9 = Teams<9, 2, 1>;
 
 constexpr uint32_t kRingMin = 65536;           // entry ring bytes (power of two; Cfg::kRing may be larger)
 constexpr uint32_t kChunk = 16384;             // bytes per bulk copy (>= 8 KB: ~7 TB/s, profiles/r01_bulk_copy_bench.txt)
-constexpr int kNRMax = 8;                      // cempty barriers reserved (ring <= 128 KB)
 // "chunk landed" barriers: chunk k uses cfull[k % kNB]. A decoder may wait for a
 // chunk up to ~9 tiles (<= 45 chunks) past the oldest unconsumed one; with more
 // barriers than that, the barrier's previous phase is always complete, so the
@@ -230,11 +229,16 @@ struct Unit {
   int rp, s, kt0, kt1;
 };
 __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
+  // 32-bit unsigned arithmetic (split * tiles_k < 2^32): a 64-bit division is a
+  // ~100-instruction subroutine and this runs per unit in every role
+  const uint32_t split = static_cast<uint32_t>(p.split), tk = static_cast<uint32_t>(p.tiles_k);
+  const uint32_t uu = static_cast<uint32_t>(u);
+  const uint32_t rp = uu / split, sidx = uu - rp * split;
   Unit x;
-  x.rp = u / p.split;
-  x.s = u - x.rp * p.split;
-  x.kt0 = static_cast<int>(static_cast<long long>(x.s) * p.tiles_k / p.split);
-  x.kt1 = static_cast<int>(static_cast<long long>(x.s + 1) * p.tiles_k / p.split);
+  x.rp = static_cast<int>(rp);
+  x.s = static_cast<int>(sidx);
+  x.kt0 = static_cast<int>(sidx * tk / split);
+  x.kt1 = static_cast<int>((sidx + 1) * tk / split);
   return x;
 }
 
@@ -478,6 +482,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
   const int ncl = static_cast<int>(num_clusters_x());
 
   if (threadIdx.x == 0) {
+    TRACE(9, 0);  // kernel start
     for (int i = 0; i < kNB; ++i) mbar_init(s.cfull + 8 * i, 1);
     for (int i = 0; i < C::kNR; ++i) mbar_init(s.cempty + 8 * i, 1);
     for (int i = 0; i < TM::kNA; ++i) {
@@ -501,6 +506,19 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
     fence_barrier_init();
   }
   if (warp == TM::kWarpX && lane == 0) prefetch_tmap(&tmap_x);
+  if (warp == TM::kWarpStream) {
+    // Pull this CTA's tile offsets into L2 while the CTA initialises: the unit
+    // validation and the metadata batches then read L2.
+    for (int u = cid + lane * ncl; u < p.units; u += 32 * ncl) {
+      const Unit un = unit_of(p, u);
+      const int rb = 2 * un.rp + static_cast<int>(rank);
+      if (rb < p.tiles_m) {
+        const uint64_t b0 = reinterpret_cast<uint64_t>(p.off + static_cast<size_t>(rb) * p.tiles_k + un.kt0) & ~15ull;
+        const uint64_t b1 = (reinterpret_cast<uint64_t>(p.off + static_cast<size_t>(rb) * p.tiles_k + un.kt1 + 1) + 15) & ~15ull;
+        bulk_prefetch_l2(reinterpret_cast<const void*>(b0), static_cast<uint32_t>(b1 - b0));
+      }
+    }
+  }
   if (warp == TM::kWarpMma) tmem_alloc_pair(s.tmem_slot, C::kTmemCols);
   for (uint32_t i = threadIdx.x; i < TM::kNA * kABytes / 16; i += TM::kThreads) sts128_zero(s.a + 16 * i);
   HB(60, 0);
@@ -610,7 +628,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
         g0 = __ldg(p.off + t0);
         g1 = __ldg(p.off + t0 + nt);
         bool bad = g0 > g1 || g1 > p.n_entries || (g0 & 31u) != 0;
-#pragma unroll 4
+#pragma unroll 16
         for (uint32_t i = lane; i < nt; i += 32) {
           const uint32_t a = __ldg(p.off + t0 + i), b = __ldg(p.off + t0 + i + 1);
           bad |= b < a || ((b - a) & 31u) != 0;
@@ -630,6 +648,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
     __syncwarp();
     if (lane == 0) {
       st_release_u32(s.tab_ready, 1u);  // unit table complete (read by the polling warp)
+      TRACE(9, 1);
       // 2. Stream.
       const uint64_t pol = policy_evict_first();
       const uint32_t nchunks = (total + kChunk - 1) / kChunk;
@@ -1018,6 +1037,9 @@ int spmm_sm100_plan(uint32_t m, uint32_t k, int n, int split_k, SpmmPlan* plan) 
   const int tiles_mp = (tiles_m + 1) / 2;
   const int cl = std::max(1, num_sms() / 2 - 4);
   while (plan->split > 1 && (tiles_mp * plan->split + cl - 1) / cl > kMaxUnits) --plan->split;
+  // the device computes unit bounds in 32 bits (unit_of)
+  while (plan->split > 1 && static_cast<uint64_t>(plan->split) * static_cast<uint64_t>(tiles_k) >= (1ull << 32))
+    --plan->split;
   plan->units = tiles_mp * plan->split;
   plan->grid = std::min(plan->units, num_sms() / 2);  // CTA pairs
   plan->smem = 0;

@@ -86,3 +86,8 @@ if os.environ.get("TRACE_CHAIN"):
         print("  %4d | %7d %9d %8d %10d %12d | %7d" % (
             i, tr[2][i] - base, tr[4][i] - tr[2][i], tr[7][i] - tr[4][i], tr[15][i] - tr[7][i],
             tr[0][i + na] - tr[15][i] if tr[0][i + na] else -1, tr[2][i] - tr[13][i]))
+if os.environ.get("TRACE_START"):
+    k0 = tr[9][0]
+    print("  kernel start -> unit table ready %d, first chunk issued %d, first meta published %d, first decode start %d,"
+          " first MMA %d, last MMA commit %d (cycles)" % (tr[9][1] - k0, tr[6][0] - k0, tr[10][0] - k0, tr[13][0] - k0,
+                                                          tr[8][0] - k0, tr[7][n - 1] - k0 if n else -1))
