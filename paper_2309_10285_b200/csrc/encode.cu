@@ -133,6 +133,32 @@ __device__ __forceinline__ Pair load_pair(const uint16_t* __restrict__ w, uint32
   return p;
 }
 
+// The two elements at (x, y0), (x, y0 + 1) as one word (v0 | v1 << 16), 0 outside.
+__device__ __forceinline__ uint32_t load_raw(const uint16_t* __restrict__ w, uint32_t k, long long r0, int c0, int x,
+                                             int y0, int x_end, int y_end) {
+  const bool val0 = x < x_end && y0 < y_end;
+  const bool val1 = x < x_end && y0 + 1 < y_end;
+  if (!val0) return 0u;
+  const uint16_t* src = w + (r0 + x) * k + c0 + y0;
+  if (val1 && ((reinterpret_cast<uintptr_t>(src) & 3u) == 0)) return __ldg(reinterpret_cast<const uint32_t*>(src));
+  return static_cast<uint32_t>(__ldg(src)) | (val1 ? static_cast<uint32_t>(__ldg(src + 1)) << 16 : 0u);
+}
+__device__ __forceinline__ Pair pair_from_raw(uint32_t raw, int y0, int k_tb) {
+  Pair p;
+  p.in0 = y0 < k_tb;
+  p.in1 = y0 + 1 < k_tb;
+  p.v0 = raw & 0xFFFFu;
+  p.v1 = raw >> 16;
+  p.nz0 = (p.v0 & 0x7FFFu) != 0;
+  p.nz1 = (p.v1 & 0x7FFFu) != 0;
+  return p;
+}
+
+// Items (rows x 64-column chunks) per warp kept in registers between the two
+// passes when the tile shape allows (128 x 64 with 8 warps): the tile is read
+// from HBM once, with all 16 loads of a warp in flight at once.
+constexpr int kEmitIpw = 16;
+
 // One block (8 warps) per tile. See the file comment for the closed form.
 __global__ void __launch_bounds__(256) encode_emit_kernel(const uint16_t* __restrict__ w, uint32_t m,
                                                           uint32_t k, int m_tb, int k_tb, int tiles_k,
@@ -159,8 +185,32 @@ __global__ void __launch_bounds__(256) encode_emit_kernel(const uint16_t* __rest
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const uint32_t lt = lanemask_lt();
 
+  const bool regs = lay.items == kEmitIpw * nwarps && nch == 1;  // the warp's items fit in registers (item = row)
+  uint32_t raw[kEmitIpw];
+  if (regs) {
+#pragma unroll
+    for (int q = 0; q < kEmitIpw; ++q) raw[q] = load_raw(w, k, r0, c0, warp + q * nwarps, 2 * lane, x_end, y_end);
+  }
+
   // ---- pass A: per (row, chunk) item, per-bank-column counts and nz / zero counts
-  for (int it = warp; it < lay.items; it += nwarps) {
+#pragma unroll
+  for (int q = 0; q < kEmitIpw; ++q) {
+    if (!regs) break;
+    const int it = warp + q * nwarps;
+    const Pair p = pair_from_raw(raw[q], 2 * lane, k_tb);
+    // per bank column j = lane % 4: nonzeros of the lanes l = j (mod 4), summed
+    // by three xor-shuffles; lane j < 4 stores byte j of cnt4[it]
+    uint32_t v = (p.nz0 ? 1u : 0u) + (p.nz1 ? 1u : 0u);
+    uint32_t zc = (p.in0 && !p.nz0 ? 1u : 0u) + (p.in1 && !p.nz1 ? 1u : 0u);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    const uint32_t nt = __reduce_add_sync(0xffffffffu, (p.nz0 ? 1u : 0u) + (p.nz1 ? 1u : 0u));
+    zc = __reduce_add_sync(0xffffffffu, zc);
+    if (lane < 4) reinterpret_cast<uint8_t*>(cnt4)[4 * it + lane] = static_cast<uint8_t>(v);
+    if (lane == 0) nzz[it] = nt | (zc << 16);
+  }
+  for (int it = warp; it < lay.items && !regs; it += nwarps) {
     const int x = it / nch, ch = it - x * nch;
     const Pair p = load_pair(w, k, r0, c0, x, ch * 64 + 2 * lane, x_end, y_end, k_tb);
     const uint32_t b0 = __ballot_sync(0xffffffffu, p.nz0), b1 = __ballot_sync(0xffffffffu, p.nz1);
@@ -184,11 +234,23 @@ __global__ void __launch_bounds__(256) encode_emit_kernel(const uint16_t* __rest
   if (warp == 0) {
     const int x0 = lane >> 2, j = lane & 3;
     uint32_t run = 0;
-    for (int x = x0; x < m_tb; x += 8) {
-      for (int ch = 0; ch < nch; ++ch) {
-        const int it = x * nch + ch;
-        bpre[it * 4 + j] = static_cast<uint16_t>(run);
-        run += (cnt4[it] >> (8 * j)) & 0xFFu;
+    if (regs && m_tb == 8 * kEmitIpw) {
+      // all 16 counts loaded first (independent LDS), then the running sum
+      uint32_t cv[kEmitIpw];
+#pragma unroll
+      for (int q = 0; q < kEmitIpw; ++q) cv[q] = reinterpret_cast<const uint8_t*>(cnt4)[4 * (x0 + 8 * q) + j];
+#pragma unroll
+      for (int q = 0; q < kEmitIpw; ++q) {
+        bpre[(x0 + 8 * q) * 4 + j] = static_cast<uint16_t>(run);
+        run += cv[q];
+      }
+    } else {
+      for (int x = x0; x < m_tb; x += 8) {
+        for (int ch = 0; ch < nch; ++ch) {
+          const int it = x * nch + ch;
+          bpre[it * 4 + j] = static_cast<uint16_t>(run);
+          run += (cnt4[it] >> (8 * j)) & 0xFFu;
+        }
       }
     }
     cb[lane] = run;
@@ -248,10 +310,7 @@ __global__ void __launch_bounds__(256) encode_emit_kernel(const uint16_t* __rest
 
   // ---- pass B: place every nonzero and the first `pad` zero positions
   uint32_t* out = lay.stage ? stg : entries + base;
-  for (int it = warp; it < lay.items; it += nwarps) {
-    const int x = it / nch, ch = it - x * nch;
-    const int y0 = ch * 64 + 2 * lane;
-    const Pair p = load_pair(w, k, r0, c0, x, y0, x_end, y_end, k_tb);
+  auto place = [&](int it, int x, int y0, const Pair& p) {
     const uint32_t b0 = __ballot_sync(0xffffffffu, p.nz0), b1 = __ballot_sync(0xffffffffu, p.nz1);
     const bool zp0 = p.in0 && !p.nz0, zp1 = p.in1 && !p.nz1;
     const uint32_t z0 = __ballot_sync(0xffffffffu, zp0), z1 = __ballot_sync(0xffffffffu, zp1);
@@ -281,6 +340,19 @@ __global__ void __launch_bounds__(256) encode_emit_kernel(const uint16_t* __rest
       const uint32_t zr1 = zr0 + (zp0 ? 1u : 0u);
       if (zp0 && zr0 < pad) out[nnz + zr0] = loc0;
       if (zp1 && zr1 < pad) out[nnz + zr1] = loc0 + 1;
+    }
+  };
+  if (regs) {
+#pragma unroll
+    for (int q = 0; q < kEmitIpw; ++q) {
+      const int it = warp + q * nwarps;
+      place(it, it, 2 * lane, pair_from_raw(raw[q], 2 * lane, k_tb));
+    }
+  } else {
+    for (int it = warp; it < lay.items; it += nwarps) {
+      const int x = it / nch, ch = it - x * nch;
+      const int y0 = ch * 64 + 2 * lane;
+      place(it, x, y0, load_pair(w, k, r0, c0, x, y0, x_end, y_end, k_tb));
     }
   }
   if (lay.stage) {
