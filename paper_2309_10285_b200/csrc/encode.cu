@@ -188,8 +188,16 @@ __global__ void __launch_bounds__(256) encode_emit_kernel(const uint16_t* __rest
   const bool regs = lay.items == kEmitIpw * nwarps && nch == 1;  // the warp's items fit in registers (item = row)
   uint32_t raw[kEmitIpw];
   if (regs) {
+    if (x_end == m_tb && y_end == 64 && (k & 1u) == 0) {
+      // full tile, 4-byte aligned rows: one strided pointer, no per-item bounds
+      const uint32_t* rp = reinterpret_cast<const uint32_t*>(w + (r0 + warp) * k + c0) + lane;
+      const size_t stride = static_cast<size_t>(nwarps) * (k >> 1);
 #pragma unroll
-    for (int q = 0; q < kEmitIpw; ++q) raw[q] = load_raw(w, k, r0, c0, warp + q * nwarps, 2 * lane, x_end, y_end);
+      for (int q = 0; q < kEmitIpw; ++q) raw[q] = __ldg(rp + q * stride);
+    } else {
+#pragma unroll
+      for (int q = 0; q < kEmitIpw; ++q) raw[q] = load_raw(w, k, r0, c0, warp + q * nwarps, 2 * lane, x_end, y_end);
+    }
   }
 
   // ---- pass A: per (row, chunk) item, per-bank-column counts and nz / zero counts
