@@ -30,6 +30,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SpMM TFLOPS (2MKN/t) + HBM GB/s, OPT-66B/175B shapes, N=8-64, 70-90% sparse"
 SHAPES = {"qkv": (27648, 9216), "out": (9216, 9216), "ffn1": (36864, 9216), "ffn2": (9216, 36864)}
+# SURVEY.md §8d C4 (side suite, --suite opt175b; the default line stays on configs[1])
+SHAPES_175B = {"qkv": (36864, 12288), "ffn1": (49152, 12288), "ffn2": (12288, 49152)}
+WORKLOAD_175B = "OPT-175B QKV/FFN1/FFN2 SpMMs x N{8,16,32,64} x sparsity{0.7,0.8,0.9} (36 per step)"
 NS = [8, 16, 32, 64]
 BETAS = [0.7, 0.8, 0.9]
 WORKLOAD = "OPT-66B QKV/out/FFN1/FFN2 SpMMs x N{8,16,32,64} x sparsity{0.7,0.8,0.9} (48 per step)"
@@ -176,7 +179,7 @@ def run_ours(args, rank, world):
         # whole step can be captured in a CUDA graph)
         t, r0, rows = mats[(name, beta)]
         y = ys[(name, beta, n)]
-        tc.spmm(t, xs[(SHAPES[name][1], n)], out=y, ws=wss[(name, beta, n)], check=False)
+        tc.spmm(t, xs[(SHAPES[name][1], n)], split_k=args.split, out=y, ws=wss[(name, beta, n)], check=False)
         if world > 1:
             full, pad = gathered[(name, beta, n)]
             pad[:rows].copy_(y[:rows])
@@ -189,7 +192,7 @@ def run_ours(args, rank, world):
     # correctness gate before timing: device error words clean, results finite
     for c in cells:
         t, r0, rows = mats[(c[0], c[1])]
-        tc.spmm(t, xs[(SHAPES[c[0]][1], c[2])], out=ys[c], ws=wss[c], check=True)
+        tc.spmm(t, xs[(SHAPES[c[0]][1], c[2])], split_k=args.split, out=ys[c], ws=wss[c], check=True)
     torch.cuda.synchronize()
 
     use_graph = not args.no_graph
@@ -231,7 +234,7 @@ def run_ours(args, rank, world):
     launches_per_step = 0
     for nm, b, n in cells:
         t = mats[(nm, b)][0]
-        launches_per_step += 1 + (tc.auto_split(t.m, t.k, n) > 1)
+        launches_per_step += 1 + ((args.split or tc.auto_split(t.m, t.k, n)) > 1)
     total_alg = sum(alg_bytes(mats[(nm, b)][0], n) for nm, b, n in cells)
 
     # ---- per-SpMM device times (L2 flushed before each), roofline of the SpMM kernel.
@@ -258,7 +261,7 @@ def run_ours(args, rank, world):
             if (nm, b, n) in cell_graphs:
                 cell_graphs[(nm, b, n)].replay()
             else:
-                tc.spmm(t, xs[(t.k, n)], out=ys[(nm, b, n)], ws=wss[(nm, b, n)], check=False)
+                tc.spmm(t, xs[(t.k, n)], split_k=args.split, out=ys[(nm, b, n)], ws=wss[(nm, b, n)], check=False)
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) * 1e3)
@@ -268,7 +271,7 @@ def run_ours(args, rank, world):
         t_hbm = nbytes / (hbm_peak * 1e3)  # us
         t_tc = fl / (tc_peak * 1e6)
         cell_rows.append({"shape": nm, "M": t.m, "K": t.k, "N": n, "sparsity": b, "E": t.n_entries,
-                          "split": tc.auto_split(t.m, t.k, n), "us": round(us, 2),
+                          "split": args.split or tc.auto_split(t.m, t.k, n), "us": round(us, 2),
                           "tflops": round(fl / us / 1e6, 2), "gbs": round(nbytes / us / 1e3, 1),
                           "hbm_frac": round(t_hbm / us, 3), "roofline_frac": round(max(t_hbm, t_tc) / us, 3)})
         sum_t += us
@@ -517,7 +520,13 @@ def main():
     ap.add_argument("--kernel-reps", type=int, default=5)
     ap.add_argument("--ref-steps", type=int, default=0)
     ap.add_argument("--ref-full", action="store_true")
+    ap.add_argument("--suite", default="opt66b", choices=["opt66b", "opt175b"],
+                    help="opt66b = BASELINE.json configs[1] (the metric's config); opt175b = SURVEY §8d C4")
+    ap.add_argument("--split", type=int, default=0, help="force split-K S (0 = auto; SURVEY §8d C3)")
     args = ap.parse_args()
+    if args.suite == "opt175b":
+        global SHAPES, WORKLOAD
+        SHAPES, WORKLOAD = SHAPES_175B, WORKLOAD_175B
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
