@@ -834,7 +834,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
           // comes right before that group's MMAs.
           const bool quad = kQuad && C::kTX == 4 && TM::kNA % 4 == 0 && (gt & 3) == 0 && in_stage == 0 &&
                             kt + 3 < un.kt1;
-          const bool two = !quad && TM::kG == 2 && (gt & 1) == 0 && kt + 1 < un.kt1 && in_stage + 1 < C::kTX;
+          const bool two = !quad && TM::kNA % 2 == 0 && (gt & 1) == 0 && kt + 1 < un.kt1 && in_stage + 1 < C::kTX;
           const uint32_t nt = quad ? 4u : (two ? 2u : 1u);
           TRACE(3, gt);
           if (gt % TM::kG == 0) mbar_wait(s.afull + 8 * (b / TM::kG), (gt / TM::kNA) & 1);  // the group's tiles
