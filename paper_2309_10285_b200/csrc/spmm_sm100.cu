@@ -110,6 +110,12 @@ using TeamsDense = Teams<TCSL_DENSE_T, 4, TCSL_DENSE_G>;
 #endif
 // N <= 16 leaves room for a ninth buffer (X stages take 16 KB instead of 32 KB)
 using TeamsSparse9 = Teams<9, 2, 1>;
+#ifndef TCSL_MID_TEAMS
+#define TCSL_MID_TEAMS 1
+#endif
+// medium density (~40-54 groups per tile, β ≈ 0.8): 8 buffers of 3-warp teams
+// (same 32 warps as the dense shape, two more tiles in flight, whole-stage issue)
+using TeamsMid = Teams<8, 3, 1>;
 
 
 constexpr uint32_t kRingMin = 65536;           // entry ring bytes (power of two; Cfg::kRing may be larger)
@@ -976,9 +982,17 @@ cudaError_t launch_shape(const Params& p, const CUtensorMap& tm, int clusters, c
 
 // Team shape for a matrix: 2-warp teams while a warp's share of a mean tile
 // (mean groups / 2) leaves headroom under kGMax, else 4-warp teams.
+double mean_groups(uint64_t n_entries, uint64_t tiles) {
+  return tiles ? static_cast<double>(n_entries) / 32.0 / static_cast<double>(tiles) : 0.0;
+}
 bool sparse_teams(uint64_t n_entries, uint64_t tiles) {
-  const double mean_groups = tiles ? static_cast<double>(n_entries) / 32.0 / static_cast<double>(tiles) : 0.0;
-  return mean_groups <= 0.8 * kGMax * TeamsSparse::kTeamWarps;
+  return mean_groups(n_entries, tiles) <= 0.8 * kGMax * TeamsSparse::kTeamWarps;
+}
+bool mid_teams(uint64_t n_entries, uint64_t tiles) {
+#ifndef TCSL_MID_MAX
+#define TCSL_MID_MAX 0.9
+#endif
+  return TCSL_MID_TEAMS && mean_groups(n_entries, tiles) <= TCSL_MID_MAX * kGMax * TeamsMid::kTeamWarps;
 }
 
 template <int NH>
@@ -988,6 +1002,7 @@ cudaError_t launch_nh(const Params& p, const CUtensorMap& tm, int clusters, cuda
     if constexpr (TCSL_SPARSE9 && NH == 8) return launch_shape<NH, TeamsSparse9>(p, tm, clusters, s);
     return launch_shape<NH, TeamsSparse>(p, tm, clusters, s);
   }
+  if (mid_teams(p.n_entries, tiles)) return launch_shape<NH, TeamsMid>(p, tm, clusters, s);
   return launch_shape<NH, TeamsDense>(p, tm, clusters, s);
 }
 
