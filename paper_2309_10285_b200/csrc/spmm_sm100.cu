@@ -60,12 +60,17 @@ constexpr uint32_t kABytes = kMTB * kKTB * 2;  // dense fp16 tile, 16 KB
 constexpr int kGMax = 20;                      // groups per warp per tile remembered for re-clearing
 
 // Decode team shape. One dense-tile buffer per team. T teams of W warps; the
-// host picks the shape from the matrix's mean groups per tile (spmm_team_shape):
-// sparse tiles are decoded by 2-warp teams (half the per-tile bookkeeping, 8
-// tiles in flight), denser ones by 4-warp teams (each warp's share of a tile
-// must fit the kGMax remembered addresses).
-template <int T, int W, int G = (T % 2 == 0) ? 2 : 1>
+// host picks the shape from the matrix's mean groups per tile (launch_nh):
+// sparse tiles (<= 32 groups) are decoded by 8 teams of 2 warps with
+// clear-by-rescatter, dense ones (<= 81) by 8 teams of 3 warps with a zero
+// fill and 28 groups per warp in registers, denser ones by 6 teams of 4 warps.
+template <int T, int W, int G = (T % 2 == 0) ? 2 : 1, int KG = kGMax, bool ZF = false>
 struct Teams {
+  // KG: groups per warp per tile kept in registers; ZF: the team zero-fills the
+  // whole 16 KB tile before each decode (no per-warp address memory) instead
+  // of re-scattering zeros at the previous tile's addresses
+  static constexpr int kGK = KG;
+  static constexpr bool kZeroFill = ZF;
   static constexpr int kTeams = T;
   static constexpr int kTeamWarps = W;
   static constexpr int kNA = T;                    // dense-tile buffers (one per team)
@@ -104,18 +109,13 @@ using TeamsSparse = Teams<8, 2, TCSL_SPARSE_G>;  // G=1, per-tile release: +2-5 
 #ifndef TCSL_DENSE_G
 #define TCSL_DENSE_G 1
 #endif
-using TeamsDense = Teams<TCSL_DENSE_T, 4, TCSL_DENSE_G>;
-#ifndef TCSL_SPARSE9
-#define TCSL_SPARSE9 0
-#endif
-// N <= 16 leaves room for a ninth buffer (X stages take 16 KB instead of 32 KB)
-using TeamsSparse9 = Teams<9, 2, 1>;
-#ifndef TCSL_MID_TEAMS
-#define TCSL_MID_TEAMS 1
-#endif
-// medium density (~40-54 groups per tile, β ≈ 0.8): 8 buffers of 3-warp teams
-// (same 32 warps as the dense shape, two more tiles in flight, whole-stage issue)
-using TeamsMid = Teams<8, 3, 1>;
+using TeamsDense = Teams<TCSL_DENSE_T, 4, TCSL_DENSE_G>;  // very dense tiles (> 81 groups, β < ~0.69)
+// Dense tiles (32-81 groups per tile, β ≈ 0.7-0.85): 8 buffers of 3-warp teams
+// keeping up to 28 groups per warp in registers, with a whole-tile zero fill
+// instead of the per-warp address memory (the registers go to the entries).
+// -13..15 % at β=0.7 and -2..5 % at β=0.8 against 6 x 4 clear-by-rescatter
+// teams (profiles/r01_ablation_mma_loop.txt, item 18).
+using TeamsDense3 = Teams<8, 3, 1, 28, true>;
 
 
 constexpr uint32_t kRingMin = 65536;           // entry ring bytes (power of two; Cfg::kRing may be larger)
@@ -286,45 +286,52 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
 #define TCSL_DOWN16(X) \
   X(15) X(14) X(13) X(12) X(11) X(10) X(9) X(8) X(7) X(6) X(5) X(4) X(3) X(2) X(1) X(0)
 #define TCSL_DOWN20(X) X(19) X(18) X(17) X(16) TCSL_DOWN16(X)
+#define TCSL_DOWN28(X) X(27) X(26) X(25) X(24) X(23) X(22) X(21) X(20) TCSL_DOWN20(X)
 
-__device__ __forceinline__ void load_groups(uint32_t (&E)[kGMax], uint32_t rbase, uint32_t cnt) {
+// Cases J >= KG are discarded at compile time (the count is clamped to KG).
+template <int KG>
+__device__ __forceinline__ void load_groups(uint32_t (&E)[KG], uint32_t rbase, uint32_t cnt) {
   switch (cnt) {
 #define TCSL_LD(J) \
   case J + 1:      \
-    E[J] = lds32(rbase + (J) * 128u); [[fallthrough]];
+    if constexpr ((J) < KG) E[(J) < KG ? (J) : 0] = lds32(rbase + (J) * 128u); [[fallthrough]];
     default:
-      TCSL_DOWN20(TCSL_LD)
+      TCSL_DOWN28(TCSL_LD)
     case 0:
       break;
 #undef TCSL_LD
   }
 }
 
-__device__ __forceinline__ void clear_groups(const uint32_t (&Z)[kGMax], uint32_t cnt) {
+template <int KG>
+__device__ __forceinline__ void clear_groups(const uint32_t (&Z)[KG], uint32_t cnt) {
   switch (cnt) {
 #define TCSL_CLR(J) \
   case J + 1:       \
-    sts16(Z[J], 0u); [[fallthrough]];
+    if constexpr ((J) < KG) sts16(Z[(J) < KG ? (J) : 0], 0u); [[fallthrough]];
     default:
-      TCSL_DOWN20(TCSL_CLR)
+      TCSL_DOWN28(TCSL_CLR)
     case 0:
       break;
 #undef TCSL_CLR
   }
 }
 
-__device__ __forceinline__ void scatter_groups(const uint32_t (&E)[kGMax], uint32_t (&Z)[kGMax], uint32_t cnt,
+// REC: remember the addresses in Z (for clear-by-rescatter)
+template <int KG, int KZ, bool REC>
+__device__ __forceinline__ void scatter_groups(const uint32_t (&E)[KG], uint32_t (&Z)[KZ], uint32_t cnt,
                                                uint32_t a_tile) {
   switch (cnt) {
-#define TCSL_SCAT(J)                                 \
-  case J + 1: {                                      \
-    const uint32_t a = a_addr(a_tile, E[J]);         \
-    sts16(a, E[J] >> 16);                            \
-    Z[J] = a;                                        \
-  }                                                  \
+#define TCSL_SCAT(J)                                             \
+  case J + 1:                                                    \
+    if constexpr ((J) < KG) {                                    \
+      const uint32_t a = a_addr(a_tile, E[(J) < KG ? (J) : 0]);  \
+      sts16(a, E[(J) < KG ? (J) : 0] >> 16);                     \
+      if constexpr (REC) Z[(J) < KZ ? (J) : 0] = a;              \
+    }                                                            \
     [[fallthrough]];
     default:
-      TCSL_DOWN20(TCSL_SCAT)
+      TCSL_DOWN28(TCSL_SCAT)
     case 0:
       break;
 #undef TCSL_SCAT
@@ -351,8 +358,10 @@ __device__ __forceinline__ void release_ring(const Smem& s, uint32_t lo, uint32_
 // what this warp last wrote into the tile's buffer.
 template <class TM, uint32_t RING>
 __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint32_t gt, int team, int tw, int lane,
-                                            uint32_t afull_leader, uint32_t total, uint32_t (&E)[kGMax],
-                                            uint32_t (&Z)[kGMax], uint32_t& nz, uint32_t& err_or, Prof& prof_) {
+                                            uint32_t afull_leader, uint32_t total, uint32_t (&E)[TM::kGK],
+                                            uint32_t (&Z)[TM::kZeroFill ? 1 : TM::kGK], uint32_t& nz,
+                                            uint32_t& err_or, Prof& prof_) {
+  constexpr int KG = TM::kGK;
   // per-tile metadata from the stream producer (normally published long ago)
   HB(1, gt);
   if (tw == 0 && lane == 0) TRACE(13, gt);
@@ -367,7 +376,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   PROF_ADD(0);
   const uint32_t g0w = meta.y * tw / TM::kTeamWarps, g1w = meta.y * (tw + 1) / TM::kTeamWarps;
   const uint32_t cnt = g1w - g0w;
-  const uint32_t ncnt = min(cnt, static_cast<uint32_t>(kGMax));
+  const uint32_t ncnt = min(cnt, static_cast<uint32_t>(KG));
   const uint32_t lo = meta.x + g0w * 128u, hi = meta.x + g1w * 128u;  // this warp's stream bytes
   HB(2, gt);
   if (cnt) {
@@ -379,18 +388,18 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
       load_groups(E, s.ring + (lo & (RING - 1)) + 4u * lane, ncnt);
     } else {  // this warp's span wraps around the ring end
 #pragma unroll
-      for (int j = 0; j < kGMax; ++j)
+      for (int j = 0; j < KG; ++j)
         if (static_cast<uint32_t>(j) < ncnt) E[j] = lds32(s.ring + ((lo + j * 128u) & (RING - 1)) + 4u * lane);
     }
     // locations must stay inside the 128x64 tile; slots past ncnt hold this
     // warp's earlier (already checked) entries
 #pragma unroll
-    for (int j = 0; j < kGMax; ++j) err_or |= E[j];
+    for (int j = 0; j < KG; ++j) err_or |= E[j];
     // the entries are in registers now (err_or consumed them): hand the ring
     // bytes back at once so the stream refills while this tile waits for its
     // buffer (holding them longer starves the ring at low sparsity)
     __syncwarp();
-    if (cnt <= static_cast<uint32_t>(kGMax) && lane == 0) release_ring<RING / kChunk>(s, lo, hi);
+    if (cnt <= static_cast<uint32_t>(KG) && lane == 0) release_ring<RING / kChunk>(s, lo, hi);
     PROF_ADD(2);
   }
   if (tw == 0 && lane == 0) TRACE(14, gt);
@@ -406,10 +415,11 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   HB(4, gt);
   // s.ovf[b] = the last tile in buffer b for which some warp of the team wrote
   // more groups than it remembers: then the whole team zeroes the tile.
-  if (gt >= static_cast<uint32_t>(TM::kNA) && lds32(s.ovf + 4 * b) == gt - TM::kNA) {
+  if (TM::kZeroFill ? gt >= static_cast<uint32_t>(TM::kNA)
+                    : (gt >= static_cast<uint32_t>(TM::kNA) && lds32(s.ovf + 4 * b) == gt - TM::kNA)) {
     for (int r = tw; r < static_cast<int>(kABytes / 512); r += TM::kTeamWarps) sts128_zero(a_tile + 512 * r + 16 * lane);
-  } else if (!DBG(1)) {
-    clear_groups(Z, nz);
+  } else if (!TM::kZeroFill && !DBG(1)) {
+    clear_groups<TM::kZeroFill ? 1 : KG>(Z, nz);
   }
   PROF_ADD(4);
   HB(5, gt);
@@ -420,17 +430,17 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
     TRACE(1, gt);
     asm volatile("red.relaxed.cta.shared::cta.add.u32 [%0], 1;" ::"r"(s.done) : "memory");  // meta slot read
   }
-  if (!DBG(1)) scatter_groups(E, Z, ncnt, a_tile);
+  if (!DBG(1)) scatter_groups<KG, TM::kZeroFill ? 1 : KG, !TM::kZeroFill>(E, Z, ncnt, a_tile);
   nz = DBG(1) ? 0 : ncnt;
-  if (cnt > static_cast<uint32_t>(kGMax)) {  // dense tiles (> ~25 % nonzeros)
-    for (uint32_t g = kGMax; g < cnt; ++g) {
+  if (cnt > static_cast<uint32_t>(KG)) {  // dense tiles (> ~25 % nonzeros)
+    for (uint32_t g = KG; g < cnt; ++g) {
       const uint32_t e = lds32(s.ring + ((lo + g * 128u) & (RING - 1)) + 4u * lane);
       err_or |= e;
       sts16(a_addr(a_tile, e), e >> 16);
     }
     if (lane == 0) st_shared_u32(s.ovf + 4 * b, gt);
   }
-  if (cnt > static_cast<uint32_t>(kGMax) && lane == 0) release_ring<RING / kChunk>(s, lo, hi);  // overflowed: read the ring until now
+  if (cnt > static_cast<uint32_t>(KG) && lane == 0) release_ring<RING / kChunk>(s, lo, hi);  // overflowed: read the ring until now
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
@@ -545,11 +555,11 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
       total += un.kt1 - un.kt0;
     }
     const uint32_t afull_leader = mapa_shared(s.afull, 0);
-    uint32_t E[kGMax];
+    uint32_t E[TM::kGK];
 #pragma unroll
-    for (int j = 0; j < kGMax; ++j) E[j] = 0u;  // slots past a tile's count keep older, checked entries
+    for (int j = 0; j < TM::kGK; ++j) E[j] = 0u;  // slots past a tile's count keep older, checked entries
     uint32_t err_or = 0;
-    uint32_t Z[kGMax];  // addresses last written to the team's buffer
+    uint32_t Z[TM::kZeroFill ? 1 : TM::kGK];  // addresses last written to the team's buffer
     uint32_t nz = 0;
     PROF_DECL(8);  // meta, chunk waits, load, buffer wake, clear, team barrier, scatter+arrive, total
 #ifdef TCSL_PROFILING
@@ -988,21 +998,17 @@ double mean_groups(uint64_t n_entries, uint64_t tiles) {
 bool sparse_teams(uint64_t n_entries, uint64_t tiles) {
   return mean_groups(n_entries, tiles) <= 0.8 * kGMax * TeamsSparse::kTeamWarps;
 }
-bool mid_teams(uint64_t n_entries, uint64_t tiles) {
-#ifndef TCSL_MID_MAX
-#define TCSL_MID_MAX 0.9
-#endif
-  return TCSL_MID_TEAMS && mean_groups(n_entries, tiles) <= TCSL_MID_MAX * kGMax * TeamsMid::kTeamWarps;
+bool dense3_teams(uint64_t n_entries, uint64_t tiles) {
+  return mean_groups(n_entries, tiles) <= 0.97 * TeamsDense3::kGK * TeamsDense3::kTeamWarps;
 }
 
 template <int NH>
 cudaError_t launch_nh(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
   const uint64_t tiles = static_cast<uint64_t>(p.tiles_m) * p.tiles_k;
   if (sparse_teams(p.n_entries, tiles)) {
-    if constexpr (TCSL_SPARSE9 && NH == 8) return launch_shape<NH, TeamsSparse9>(p, tm, clusters, s);
     return launch_shape<NH, TeamsSparse>(p, tm, clusters, s);
   }
-  if (mid_teams(p.n_entries, tiles)) return launch_shape<NH, TeamsMid>(p, tm, clusters, s);
+  if (dense3_teams(p.n_entries, tiles)) return launch_shape<NH, TeamsDense3>(p, tm, clusters, s);
   return launch_shape<NH, TeamsDense>(p, tm, clusters, s);
 }
 
