@@ -52,6 +52,28 @@ def test_block_multiple_shapes(port, n, beta):
     run_case(port, 512, 448, n, beta, 100 + n)
 
 
+@pytest.mark.parametrize("beta", [0.5, 0.6, 0.75, 0.85, 0.95])
+def test_team_shapes(port, beta):
+    # every decode-team shape (8x2 rescatter <= 32 groups/tile, 8x3 zero fill <= 81,
+    # 6x4 rescatter above) and the register-overflow paths
+    run_case(port, 640, 1024, 16, beta, 900 + int(beta * 100))
+
+
+def test_mixed_density_overflow(port):
+    # mean groups/tile in the 8x3 zero-fill range, but half the tiles hold ~128 groups
+    # (more than the 3 x 28 kept in registers: overflow scatter from the ring)
+    import paper_2309_10285_b200 as tc
+    a = np.vstack([port.gen_random_sparse(256, 512, 0.5, 41), port.gen_random_sparse(256, 512, 0.97, 42)])
+    x = port.gen_random_sparse(512, 32, 0.0, 43)
+    t = tc.encode(_dev(a))
+    groups = (t.n_entries / 32) / ((512 // 128) * (512 // 64))
+    assert 32 < groups <= 81, groups
+    y = tc.spmm(t, _dev(x)).cpu().numpy()
+    want = port.spmm(port.encode(a), x, 8)
+    bound = port.spmm(port.encode(a & 0x7FFF), x & 0x7FFF, 8)
+    check_tolerance(y, want, bound)
+
+
 @pytest.mark.parametrize("n", [1, 3, 5, 8, 12, 24, 40, 100, 256, 300])
 def test_ragged_shapes_and_n(port, n):
     run_case(port, 701, 333, n, 0.8, 7 * n)
