@@ -117,7 +117,15 @@ def ncu_traffic():
     """DRAM bytes per launch of the SpMM kernel from the newest committed ncu --set full
     summary (profiles/*_ncu_*.json, written by tools/ncu_summary.py), or None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_*.json")), key=os.path.getmtime)
+    import re
+
+    def version(path):  # r01_ncu_v15_ffn1_b08_n16.json -> 15 (file mtimes do not survive copies)
+        m = re.search(r"_v(\d+)[a-z]?_", os.path.basename(path))
+        return int(m.group(1)) if m else -1
+
+    files = glob.glob(os.path.join(ROOT, "profiles", "*_ncu_*.json"))
+    ref = [f for f in files if "_ffn1_b08_n16" in f]  # the reference cell of the summaries
+    files = sorted(ref or files, key=version)
     if not files:
         return None
     try:
