@@ -21,7 +21,17 @@
  *   tcsl_cuda_spmm_exact         <- tcsl::spmm bit-exact mode (dense_gemm_ref order,
  *                                   proj/src/gemm.cpp:36-40), any TileConfig
  *   tcsl_cuda_validate           <- check_offsets     proj/src/tcsl_format.cpp:19-32
+ *   tcsl_cuda_validate_entries   <- check_offsets + decode's per-entry checks
+ *                                   (location range, fringe payload, tcsl_format.cpp:137-152)
+ *   tcsl_cuda_parse_header /     <- deserialize_tcsl  proj/src/tcsl_format.cpp:180-222
+ *   tcsl_cuda_ingest                (host header checks, pinned upload, device validation)
+ *   tcsl_cuda_spmm_ex            <- tcsl::spmm + the CLI's --out-f16 narrowing
+ *                                   (tcsl_main.cpp:182-186, f16_from_f32 half.cpp:10-40),
+ *                                   with an optional per-row bias and activation
+ *   tcsl_cuda_prune_magnitude    <- prune_magnitude   proj/src/matrix.cpp:69-100
  *   tcsl_cuda_rebase_offsets     <- row-shard slicing
+ *   tcsl_cuda_allgather_rows     <- the multi-GPU exchange of SURVEY.md §8(b)/(e)
+ *                                   (the reference is single-process)
  */
 #ifndef TCSL_CUDA_H
 #define TCSL_CUDA_H
@@ -33,7 +43,7 @@
 extern "C" {
 #endif
 
-#define TCSL_CUDA_ABI_VERSION 1
+#define TCSL_CUDA_ABI_VERSION 2
 
 enum {
   TCSL_STATUS_OK = 0,
@@ -79,17 +89,74 @@ int tcsl_cuda_decode(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_
 int tcsl_cuda_validate(const uint32_t* dOffsets, uint64_t n_entries, uint32_t m, uint32_t k, int m_tb,
                        int k_tb, int* dErr, void* stream);
 
+/* Whole-matrix validation on the device (offsets AND entries), one pass over E.
+ *   mode TCSL_CHECK_DECODE:  the checks tcsl::decode makes (check_offsets, location
+ *                            < m_tb*k_tb, no nonzero value in the padded fringe) raise
+ *                            inconsistent_offsets / location_out_of_range in *dErr.
+ *   mode TCSL_CHECK_SPMM:    the checks tcsl::spmm makes (engine.cpp:8-25: each tile's
+ *                            span inside [0, n_entries], locations in range).
+ *   mode TCSL_CHECK_INGEST:  the checks deserialize_tcsl makes (check_offsets only);
+ *                            per-entry problems are reported as flags, not errors.
+ * *dFlags (device, zero it first) |= TCSL_FLAG_* in every mode. */
+enum { TCSL_CHECK_SPMM = 0, TCSL_CHECK_DECODE = 1, TCSL_CHECK_INGEST = 2 };
+#define TCSL_FLAG_DUPLICATE_LOCATIONS 1u /* a tile repeats a location (the last entry wins) */
+#define TCSL_FLAG_PARTIAL_GROUPS 2u      /* a tile span is not whole 32-entry groups */
+#define TCSL_FLAG_FRINGE_PAYLOAD 4u      /* a nonzero value sits in the padded fringe */
+#define TCSL_FLAG_LOCATION_RANGE 8u      /* a location >= m_tb * k_tb */
+int tcsl_cuda_validate_entries(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries,
+                               uint32_t m, uint32_t k, int m_tb, int k_tb, int mode, uint32_t* dFlags,
+                               int* dErr, void* stream);
+
+/* ---------------------------------------------------------------- ingest */
+/* TCSL container -> device (reference byte layout, tcsl_format.hpp:68-71).
+ * tcsl_cuda_parse_header runs deserialize_tcsl's host-side checks in its order
+ * (bad_magic, bad_version, bad_header, truncated / trailing_data from the sizes)
+ * and fills *out. tcsl_cuda_ingest then copies the offset table and the entries
+ * from `bytes` (host memory; pageable data is staged through `staging`, a pinned
+ * buffer of staging_bytes >= 1 MiB, or pass bytes already pinned and staging =
+ * NULL) into dOffsets[num_tiles + 1] / dEntries[n_entries] (16-byte aligned) and
+ * validates them on the device with TCSL_CHECK_INGEST. */
+typedef struct tcsl_cuda_header {
+  uint32_t m, k, m_tb, k_tb, num_tiles, reordered;
+  uint64_t n_entries;
+} tcsl_cuda_header;
+int tcsl_cuda_parse_header(const void* bytes, size_t size, tcsl_cuda_header* out);
+int tcsl_cuda_ingest(const void* bytes, size_t size, const tcsl_cuda_header* h, uint32_t* dOffsets,
+                     uint32_t* dEntries, void* staging, size_t staging_bytes, uint32_t* dFlags, int* dErr,
+                     void* stream);
+
 /* ------------------------------------------------------------------ spmm */
 /* Y[m x n] (fp32, row-major, ld = n) = W_tcsl x X[k x n] (binary16, row-major,
  * ld = n). Tensor-core path (tcgen05, fp32 accumulate) for TileConfig
  * {128, 64}; any other TileConfig runs the bit-exact CUDA-core path.
  * split_k: 0 = automatic, 1 = none, S > 1 = S partial sums reduced in fixed
- * order by tcsl_cuda_splitk_reduce (deterministic). */
+ * order by tcsl_cuda_splitk_reduce (deterministic).
+ * Preconditions of the tensor-core path (tcsl::encode output always meets
+ * them; tcsl_cuda_validate_entries reports violations as flags):
+ *   - every tile span is whole 32-entry groups (else inconsistent_offsets);
+ *     tcsl_cuda_spmm_exact accepts partial groups like the reference;
+ *   - no location repeats inside a tile (TCSL_FLAG_DUPLICATE_LOCATIONS): for
+ *     such inputs use tcsl_cuda_spmm_exact, which resolves them last-writer-wins
+ *     like tcsl::extract_tile (the tensor-core scatter would race);
+ *   - dEntries is 16-byte aligned (bulk copies), else invalid_argument. */
 int tcsl_cuda_spmm_workspace(uint32_t m, uint32_t k, int m_tb, int k_tb, int n, int split_k,
                              size_t* ws_bytes);
 int tcsl_cuda_spmm(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m,
                    uint32_t k, int m_tb, int k_tb, const uint16_t* dX, int n, float* dY, int split_k,
                    void* ws, size_t ws_bytes, int* dErr, void* stream);
+/* Fused epilogue: Y = act(W x X + bias) stored as fp32 or as binary16 bits
+ * narrowed round-to-nearest-even with the canonical NaN 0x7E00 (f16_from_f32,
+ * half.cpp:10-40; the CLI's --out-f16, tcsl_main.cpp:182-186). dBias: m floats
+ * (one per output row) or NULL. activation: TCSL_ACT_*. out_dtype: TCSL_OUT_*.
+ * exact != 0 runs the bit-exact CUDA-core product first (any TileConfig). */
+enum { TCSL_ACT_NONE = 0, TCSL_ACT_RELU = 1, TCSL_ACT_GELU_TANH = 2 };
+enum { TCSL_OUT_F32 = 0, TCSL_OUT_F16 = 1 };
+int tcsl_cuda_spmm_ex_workspace(uint32_t m, uint32_t k, int m_tb, int k_tb, int n, int split_k, int exact,
+                                size_t* ws_bytes);
+int tcsl_cuda_spmm_ex(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m,
+                      uint32_t k, int m_tb, int k_tb, const uint16_t* dX, int n, void* dY, int out_dtype,
+                      const float* dBias, int activation, int split_k, int exact, void* ws, size_t ws_bytes,
+                      int* dErr, void* stream);
 /* The split the automatic heuristic picks for this shape on this device. */
 int tcsl_cuda_spmm_auto_split(uint32_t m, uint32_t k, int n);
 /* Y = sum_{s=0}^{S-1} P[s] in ascending s (P is S x count floats). */
@@ -101,10 +168,33 @@ int tcsl_cuda_spmm_exact(const uint32_t* dOffsets, const uint32_t* dEntries, uin
                          uint32_t m, uint32_t k, int m_tb, int k_tb, const uint16_t* dX, int n, float* dY,
                          void* ws, size_t ws_bytes, int* dErr, void* stream);
 
+/* ------------------------------------------------------------------ prune */
+/* Magnitude pruning on the device, bit-exact with prune_magnitude: the
+ * floor(beta * count) elements smallest by |value| (NaN ranks as +inf) become
+ * +0.0; among equal magnitudes the larger row-major index goes first. dOut may
+ * equal dA. beta outside [0, 1] -> invalid_argument. */
+int tcsl_cuda_prune_workspace(uint64_t count, size_t* ws_bytes);
+int tcsl_cuda_prune_magnitude(const uint16_t* dA, uint64_t count, double beta, uint16_t* dOut, void* ws,
+                              size_t ws_bytes, void* stream);
+
 /* --------------------------------------------------------------- sharding */
 /* Row shard [tile row tr0, tr1): dOut[i] = dOffsets[tr0*tk + i] - dOffsets[tr0*tk],
  * i in [0, (tr1-tr0)*tk]. The shard's entries are dEntries + dOffsets[tr0*tk]. */
 int tcsl_cuda_rebase_offsets(const uint32_t* dOffsets, uint32_t tile0, uint32_t tile1, uint32_t* dOut,
+                             void* stream);
+
+/* Row-sharded Y: rank r holds rows [r*rows_per_rank, ...) of
+ * the m x n fp32 result in dYg (rows_per_rank x n); after the call every rank
+ * holds the whole dY (nranks*rows_per_rank x n, rank-major). One
+ * ncclAllGather on `comm` (an ncclComm_t) over NVLink, stream-ordered.
+ * NCCL is resolved at run time (dlopen "libnccl.so.2", the copy torch already
+ * loaded when there is one), so the library itself has no NCCL dependency.
+ * out_dtype TCSL_OUT_F16 gathers binary16 rows (half the bytes). */
+int tcsl_cuda_nccl_available(void);
+int tcsl_cuda_nccl_unique_id(void* id128);
+int tcsl_cuda_nccl_comm_init(void** comm, int nranks, const void* id128, int rank);
+int tcsl_cuda_nccl_comm_destroy(void* comm);
+int tcsl_cuda_allgather_rows(const void* dYg, void* dY, size_t rows_per_rank, int n, int out_dtype, void* comm,
                              void* stream);
 
 /* ------------------------------------------------------- memory plumbing */

@@ -21,9 +21,9 @@ LIB_PATH = os.path.join(LIB_DIR, "libtcsl_cuda.so")
 if os.environ.get("TCSL_CUDA_LIB"):  # A/B experiments (tools/build_variant.py); still the CUDA library
     LIB_PATH = os.path.abspath(os.environ["TCSL_CUDA_LIB"])
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["encode.cu", "misc.cu", "spmm_sm100.cu", "capi.cu"]
+SOURCES = ["encode.cu", "misc.cu", "prune.cu", "spmm_sm100.cu", "capi.cu", "nccl_rows.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared"]
+              "-Xcompiler", "-fPIC", "-shared", "-ldl"]
 
 ERRC = ["bad_magic", "bad_version", "bad_header", "bad_dtype", "truncated", "trailing_data",
         "inconsistent_offsets", "location_out_of_range", "dimension_mismatch", "invalid_argument",
@@ -47,20 +47,47 @@ class TcslError(RuntimeError):
 
 
 def build(verbose: bool = False) -> str:
-    """Compile csrc/*.cu for sm_100a into _lib/libtcsl_cuda.so (in-tree)."""
-    os.makedirs(LIB_DIR, exist_ok=True)
-    srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    newest = max(os.path.getmtime(p) for p in srcs + [os.path.join(CSRC, "sm100_ptx.cuh"),
-                                                        os.path.join(CSRC, "tcsl_internal.cuh"),
-                                                        os.path.join(HERE, "..", "include", "tcsl_cuda.h")])
-    if os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
-        return LIB_PATH
-    tmp = LIB_PATH + ".tmp"
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", tmp, *srcs]
-    subprocess.run(cmd, check=True, capture_output=not verbose)
-    os.replace(tmp, LIB_PATH)
+    """Compile csrc/*.cu for sm_100a into _lib/libtcsl_cuda.so (in-tree). Each source
+    is compiled to its own object (in parallel, only when it or a header changed),
+    then linked."""
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(os.path.join(LIB_DIR, "obj"), exist_ok=True)
+    headers = [os.path.join(CSRC, "sm100_ptx.cuh"), os.path.join(CSRC, "tcsl_internal.cuh"),
+               os.path.join(HERE, "..", "include", "tcsl_cuda.h")]
+    hdr_time = max(os.path.getmtime(h) for h in headers)
+    objs, todo = [], []
+    for src in SOURCES:
+        sp = os.path.join(CSRC, src)
+        obj = os.path.join(LIB_DIR, "obj", src.replace(".cu", ".o"))
+        objs.append(obj)
+        if not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(sp), hdr_time):
+            todo.append((sp, obj))
+    flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-ldl")]
+
+    def compile_one(job):
+        sp, obj = job
+        subprocess.run(["nvcc", *flags, "-c", "-o", obj + ".tmp", sp], check=True, capture_output=not verbose)
+        os.replace(obj + ".tmp", obj)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        list(ex.map(compile_one, todo))
+    if todo or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(os.path.getmtime(o) for o in objs):
+        tmp = LIB_PATH + ".tmp"
+        subprocess.run(["nvcc", *NVCC_FLAGS, "-o", tmp, *objs], check=True, capture_output=not verbose)
+        os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
+
+class Header(C.Structure):
+    """tcsl_cuda_header (include/tcsl_cuda.h)."""
+    _fields_ = [("m", C.c_uint32), ("k", C.c_uint32), ("m_tb", C.c_uint32), ("k_tb", C.c_uint32),
+                ("num_tiles", C.c_uint32), ("reordered", C.c_uint32), ("n_entries", C.c_uint64)]
+
+
+# include/tcsl_cuda.h constants
+CHECK_SPMM, CHECK_DECODE, CHECK_INGEST = 0, 1, 2
+FLAG_DUPLICATE_LOCATIONS, FLAG_PARTIAL_GROUPS, FLAG_FRINGE_PAYLOAD, FLAG_LOCATION_RANGE = 1, 2, 4, 8
+ACTIVATIONS = {None: 0, "none": 0, "relu": 1, "gelu_tanh": 2}
 
 _lib = None
 
@@ -99,6 +126,19 @@ def lib() -> C.CDLL:
         "tcsl_cuda_memset": ([vp, i32, sz, vp], i32),
         "tcsl_cuda_stream_sync": ([vp], i32),
         "tcsl_cuda_device_count": ([C.POINTER(i32)], i32),
+        "tcsl_cuda_validate_entries": ([vp, vp, u64, u32, u32, i32, i32, i32, vp, vp, vp], i32),
+        "tcsl_cuda_parse_header": ([vp, sz, C.POINTER(Header)], i32),
+        "tcsl_cuda_ingest": ([vp, sz, C.POINTER(Header), vp, vp, vp, sz, vp, vp, vp], i32),
+        "tcsl_cuda_spmm_ex_workspace": ([u32, u32, i32, i32, i32, i32, i32, C.POINTER(sz)], i32),
+        "tcsl_cuda_spmm_ex": ([vp, vp, u64, u32, u32, i32, i32, vp, i32, vp, i32, vp, i32, i32, i32, vp, sz, vp,
+                               vp], i32),
+        "tcsl_cuda_prune_workspace": ([u64, C.POINTER(sz)], i32),
+        "tcsl_cuda_prune_magnitude": ([vp, u64, C.c_double, vp, vp, sz, vp], i32),
+        "tcsl_cuda_nccl_available": ([], i32),
+        "tcsl_cuda_nccl_unique_id": ([vp], i32),
+        "tcsl_cuda_nccl_comm_init": ([C.POINTER(vp), i32, vp, i32], i32),
+        "tcsl_cuda_nccl_comm_destroy": ([vp], i32),
+        "tcsl_cuda_allgather_rows": ([vp, vp, sz, i32, i32, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -115,7 +155,10 @@ EXPORTED_SYMBOLS = [
     "tcsl_cuda_splitk_reduce", "tcsl_cuda_spmm_exact_workspace", "tcsl_cuda_spmm_exact",
     "tcsl_cuda_rebase_offsets", "tcsl_cuda_gen_synthetic", "tcsl_cuda_malloc", "tcsl_cuda_free",
     "tcsl_cuda_memcpy_h2d", "tcsl_cuda_memcpy_d2h", "tcsl_cuda_memset", "tcsl_cuda_stream_sync",
-    "tcsl_cuda_device_count",
+    "tcsl_cuda_device_count", "tcsl_cuda_validate_entries", "tcsl_cuda_parse_header", "tcsl_cuda_ingest",
+    "tcsl_cuda_spmm_ex_workspace", "tcsl_cuda_spmm_ex", "tcsl_cuda_prune_workspace", "tcsl_cuda_prune_magnitude",
+    "tcsl_cuda_nccl_available", "tcsl_cuda_nccl_unique_id", "tcsl_cuda_nccl_comm_init",
+    "tcsl_cuda_nccl_comm_destroy", "tcsl_cuda_allgather_rows",
 ]
 
 
@@ -164,6 +207,10 @@ class TcslMatrix:
     reordered: bool
     offsets: object
     entries: object
+    # True when every tile span is whole 32-entry groups and no location repeats
+    # inside a tile (what encode() emits): the tensor-core path's preconditions.
+    # None = not known yet: spmm() validates on the device once and caches it.
+    tc_ready: bool | None = None
 
     @property
     def tiles_m(self) -> int:
@@ -196,15 +243,19 @@ class TcslMatrix:
         ent = torch.from_numpy(np.ascontiguousarray(entries, dtype=np.uint32).view(np.int32)).to(device)
         return TcslMatrix(int(m), int(k), cfg or TileConfig(), bool(reordered), off, ent)
 
+    def shares_storage(self, other: "TcslMatrix") -> bool:
+        return self.offsets.data_ptr() == other.offsets.data_ptr() and self.entries.data_ptr() == other.entries.data_ptr()
+
 
 def _as_u16(w):
+    """binary16 operands only (the reference API is Eigen::half): float16 values, or
+    int16/uint16 tensors holding binary16 bit patterns. bfloat16 is rejected (its
+    bits would be misread as binary16)."""
     torch = _torch()
-    if w.dtype in (torch.float16, torch.bfloat16, torch.int16):
-        w = w.view(torch.int16)
-    elif w.dtype == torch.uint16:
+    if w.dtype in (torch.float16, torch.int16, torch.uint16):
         w = w.view(torch.int16)
     else:
-        raise TcslError(10, f"expected a 16-bit tensor, got {w.dtype}")
+        raise TcslError(10, f"expected binary16 (float16, or int16/uint16 bit patterns), got {w.dtype}")
     if not w.is_cuda:
         raise TcslError(10, "tensor must be on the GPU")
     return w.contiguous()
@@ -231,12 +282,14 @@ def encode(w, cfg: TileConfig | None = None, reorder: bool = True) -> TcslMatrix
     _check(L.tcsl_cuda_encode_emit(_ptr(w), m, k, cfg.m_tb, cfg.k_tb, int(reorder), _ptr(off), _ptr(ent),
                                    _ptr(err), s))
     _check(L.tcsl_cuda_read_error(_ptr(err), s), "encode")
-    return TcslMatrix(m, k, cfg, reorder, off, ent)
+    return TcslMatrix(m, k, cfg, reorder, off, ent, tc_ready=True)
 
 
 def decode(t: TcslMatrix):
     """TcslMatrix -> dense binary16 bits [m, k] as int16 (tcsl::decode)."""
     torch = _torch()
+    if t.offsets.numel() != t.num_tiles + 1:
+        raise TcslError(7, "offset table must have num_tiles+1 entries")
     L, s = lib(), _stream()
     out = torch.empty((t.m, t.k), dtype=torch.int16, device=t.offsets.device)
     err = torch.zeros(1, dtype=torch.int32, device=t.offsets.device)
@@ -247,6 +300,7 @@ def decode(t: TcslMatrix):
 
 
 def validate(t: TcslMatrix) -> None:
+    """check_offsets (proj/src/tcsl_format.cpp:19-32) on the device."""
     torch = _torch()
     L, s = lib(), _stream()
     err = torch.zeros(1, dtype=torch.int32, device=t.offsets.device)
@@ -254,6 +308,28 @@ def validate(t: TcslMatrix) -> None:
         raise TcslError(7, "offset table must have num_tiles+1 entries")
     _check(L.tcsl_cuda_validate(_ptr(t.offsets), t.n_entries, t.m, t.k, t.cfg.m_tb, t.cfg.k_tb, _ptr(err), s))
     _check(L.tcsl_cuda_read_error(_ptr(err), s), "validate")
+
+
+def check_entries(t: TcslMatrix, mode: int = CHECK_DECODE) -> int:
+    """Whole-matrix validation on the device (tcsl_cuda_validate_entries): raises
+    the reference's error class for `mode`'s checks and returns the TCSL_FLAG_* bits."""
+    torch = _torch()
+    L, s = lib(), _stream()
+    if t.offsets.numel() != t.num_tiles + 1:
+        raise TcslError(7, "offset table must have num_tiles+1 entries")
+    buf = torch.zeros(2, dtype=torch.int32, device=t.offsets.device)  # [error, flags]
+    _check(L.tcsl_cuda_validate_entries(_ptr(t.offsets), _ptr(t.entries), t.n_entries, t.m, t.k, t.cfg.m_tb,
+                                        t.cfg.k_tb, mode, C.c_void_p(buf.data_ptr() + 4), _ptr(buf), s))
+    _check(L.tcsl_cuda_read_error(_ptr(buf), s), "validate")
+    return int(buf[1].item())
+
+
+def _tc_ready(t: TcslMatrix) -> bool:
+    """The tensor-core path's preconditions (include/tcsl_cuda.h), checked once per matrix."""
+    if t.tc_ready is None:
+        flags = check_entries(t, CHECK_SPMM)
+        t.tc_ready = not (flags & (FLAG_DUPLICATE_LOCATIONS | FLAG_PARTIAL_GROUPS)) and t.entries.data_ptr() % 16 == 0
+    return t.tc_ready
 
 
 class SpmmWorkspace:
@@ -276,10 +352,16 @@ _default_ws = SpmmWorkspace()
 
 
 def spmm(t: TcslMatrix, x, split_k: int = 0, exact: bool = False, out=None, ws: SpmmWorkspace | None = None,
-         check: bool = True):
-    """Y[m, n] fp32 = t @ X[k, n] (X binary16 on the GPU). tcsl::spmm semantics.
+         check: bool = True, bias=None, activation: str | None = None, out_dtype=None):
+    """Y[m, n] = t @ X[k, n] (X binary16 on the GPU). tcsl::spmm semantics.
 
-    exact=True runs the bit-exact CUDA-core mode (dense_gemm_ref order)."""
+    exact=True runs the bit-exact CUDA-core mode (dense_gemm_ref order). Inputs
+    outside the tensor-core path's preconditions (repeated locations inside a
+    tile, spans that are not whole 32-entry groups — both legal for the
+    reference's spmm, engine.cpp:8-25) also take the exact path. Optional fused
+    epilogue: Y = activation(W X + bias) (bias: fp32 [m]; activation None /
+    "relu" / "gelu_tanh"), returned as float32 or, with out_dtype=torch.float16,
+    narrowed like f16_from_f32 (proj/src/half.cpp:10-40)."""
     torch = _torch()
     if x.dim() != 2 or x.shape[0] == 0 or x.shape[1] == 0:
         raise TcslError(10, "B must be non-empty")
@@ -287,26 +369,38 @@ def spmm(t: TcslMatrix, x, split_k: int = 0, exact: bool = False, out=None, ws: 
         raise TcslError(9, f"A has {t.k} columns, B has {x.shape[0]} rows")
     x = _as_u16(x)
     n = x.shape[1]
-    L, s = lib(), _stream()
     dev = t.offsets.device
+    if x.device != dev or t.entries.device != dev:
+        raise TcslError(10, "A and B must be on the same device")
+    if t.offsets.numel() != t.num_tiles + 1:
+        raise TcslError(7, "offset table must have num_tiles+1 entries")
+    if activation not in ACTIVATIONS:
+        raise TcslError(10, f"unknown activation {activation!r}")
+    act = ACTIVATIONS[activation]
+    out_dtype = out_dtype or (out.dtype if out is not None else torch.float32)
+    if out_dtype not in (torch.float32, torch.float16):
+        raise TcslError(10, f"output dtype must be float32 or float16, got {out_dtype}")
+    f16 = out_dtype == torch.float16
     if out is None:
-        out = torch.empty((t.m, n), dtype=torch.float32, device=dev)
+        out = torch.empty((t.m, n), dtype=out_dtype, device=dev)
+    elif (tuple(out.shape) != (t.m, n) or out.dtype != out_dtype or not out.is_contiguous()
+          or out.device != dev):
+        raise TcslError(10, f"out must be a contiguous {out_dtype} tensor of shape ({t.m}, {n}) on {dev}")
+    if bias is not None:
+        if bias.dtype != torch.float32 or bias.numel() != t.m or bias.device != dev or not bias.is_contiguous():
+            raise TcslError(10, f"bias must be a contiguous float32 tensor of {t.m} elements on {dev}")
+    if not exact and t.cfg.m_tb == 128 and t.cfg.k_tb == 64 and not _tc_ready(t):
+        exact = True
+    L, s = lib(), _stream()
     ws = ws or _default_ws
     nb = C.c_size_t()
-    if exact:
-        _check(L.tcsl_cuda_spmm_exact_workspace(t.m, t.k, C.byref(nb)))
-    else:
-        _check(L.tcsl_cuda_spmm_workspace(t.m, t.k, t.cfg.m_tb, t.cfg.k_tb, n, split_k, C.byref(nb)))
+    _check(L.tcsl_cuda_spmm_ex_workspace(t.m, t.k, t.cfg.m_tb, t.cfg.k_tb, n, split_k, int(exact), C.byref(nb)))
     buf, err = ws.get(nb.value, dev)
     if check:
         err.zero_()
-    fn = L.tcsl_cuda_spmm_exact if exact else L.tcsl_cuda_spmm
-    args = [_ptr(t.offsets), _ptr(t.entries), t.n_entries, t.m, t.k, t.cfg.m_tb, t.cfg.k_tb, _ptr(x), n,
-            _ptr(out)]
-    if not exact:
-        args.append(split_k)
-    args += [_ptr(buf), buf.numel(), _ptr(err), s]
-    _check(fn(*args), "spmm")
+    _check(L.tcsl_cuda_spmm_ex(_ptr(t.offsets), _ptr(t.entries), t.n_entries, t.m, t.k, t.cfg.m_tb, t.cfg.k_tb,
+                               _ptr(x), n, _ptr(out), int(f16), _ptr(bias), act, split_k, int(exact), _ptr(buf),
+                               buf.numel(), _ptr(err), s), "spmm")
     if check:
         _check(L.tcsl_cuda_read_error(_ptr(err), s), "spmm")
     return out
@@ -328,7 +422,7 @@ def shard_rows(t: TcslMatrix, tr0: int, tr1: int) -> TcslMatrix:
     lo = int(t.offsets[t0].item()) & 0xFFFFFFFF
     hi = int(t.offsets[t1].item()) & 0xFFFFFFFF
     rows = min(t.m, tr1 * t.cfg.m_tb) - tr0 * t.cfg.m_tb
-    return TcslMatrix(rows, t.k, t.cfg, t.reordered, off, t.entries[lo:hi])
+    return TcslMatrix(rows, t.k, t.cfg, t.reordered, off, t.entries[lo:hi], tc_ready=t.tc_ready)
 
 
 def gen_synthetic(rows: int, cols: int, beta: float, seed: int, device="cuda"):
@@ -337,3 +431,104 @@ def gen_synthetic(rows: int, cols: int, beta: float, seed: int, device="cuda"):
     w = torch.empty((rows, cols), dtype=torch.int16, device=device)
     _check(lib().tcsl_cuda_gen_synthetic(_ptr(w), rows * cols, float(beta), seed & (2**64 - 1), _stream()))
     return w
+
+
+# ------------------------------------------------------------------ TCSL container ingest
+def load_tcsl(path_or_bytes, device="cuda") -> TcslMatrix:
+    """deserialize_tcsl (proj/src/tcsl_format.cpp:180-222) straight to the device:
+    host header checks, pinned-staging upload, structural validation on the GPU
+    (no host check_offsets pass). The matrix's tensor-core readiness (no repeated
+    locations, whole groups) comes from the same device pass."""
+    import numpy as np
+    torch = _torch()
+    if isinstance(path_or_bytes, (bytes, bytearray, memoryview)):
+        data = np.frombuffer(path_or_bytes, dtype=np.uint8)
+    else:
+        data = np.fromfile(path_or_bytes, dtype=np.uint8)
+    L, s = lib(), _stream()
+    h = Header()
+    _check(L.tcsl_cuda_parse_header(C.c_void_p(data.ctypes.data) if data.size else None, data.size, C.byref(h)),
+           "deserialize")
+    dev = torch.device(device)
+    off = torch.empty(h.num_tiles + 1, dtype=torch.int32, device=dev)
+    ent = torch.empty(max(h.n_entries, 1), dtype=torch.int32, device=dev)[: h.n_entries]
+    staging = torch.empty(8 << 20, dtype=torch.uint8).pin_memory()
+    buf = torch.zeros(2, dtype=torch.int32, device=dev)  # [error, flags]
+    _check(L.tcsl_cuda_ingest(C.c_void_p(data.ctypes.data), data.size, C.byref(h), _ptr(off),
+                              C.c_void_p(ent.data_ptr()), C.c_void_p(staging.data_ptr()), staging.numel(),
+                              C.c_void_p(buf.data_ptr() + 4), _ptr(buf), s), "deserialize")
+    _check(L.tcsl_cuda_read_error(_ptr(buf), s), "deserialize")
+    flags = int(buf[1].item())
+    cfg = TileConfig(int(h.m_tb), int(h.k_tb))
+    t = TcslMatrix(int(h.m), int(h.k), cfg, bool(h.reordered), off, ent)
+    t.tc_ready = not (flags & (FLAG_DUPLICATE_LOCATIONS | FLAG_PARTIAL_GROUPS | FLAG_LOCATION_RANGE))
+    t.ingest_flags = flags
+    return t
+
+
+def serialize_tcsl(t: TcslMatrix) -> bytes:
+    """serialize_tcsl (proj/src/tcsl_format.cpp:157-178) of a device matrix: the
+    reference's byte layout (28-byte header, offsets, entries)."""
+    import struct
+    validate(t)
+    off, ent = t.to_host()
+    head = b"TCSL" + struct.pack("<HHIIIII", 1, 1 if t.reordered else 0, t.m, t.k, t.cfg.m_tb, t.cfg.k_tb,
+                                 t.num_tiles)
+    return head + off.tobytes() + ent.tobytes()
+
+
+# ------------------------------------------------------------------ pruning
+def prune_magnitude(w, beta: float, out=None):
+    """prune_magnitude (proj/src/matrix.cpp:69-100) on the GPU: the floor(beta*n)
+    smallest-magnitude elements become +0.0 (ties: larger index first). Returns
+    binary16 bits as int16 (out may alias w)."""
+    torch = _torch()
+    w = _as_u16(w)
+    n = w.numel()
+    if out is None:
+        out = torch.empty_like(w)
+    L, s = lib(), _stream()
+    nb = C.c_size_t()
+    _check(L.tcsl_cuda_prune_workspace(n, C.byref(nb)))
+    ws = torch.empty(max(nb.value, 256), dtype=torch.uint8, device=w.device)
+    _check(L.tcsl_cuda_prune_magnitude(_ptr(w), n, float(beta), _ptr(out), _ptr(ws), ws.numel(), s), "prune")
+    return out
+
+
+# ------------------------------------------------------------------ multi-GPU (NCCL via the C-ABI)
+class RowComm:
+    """An NCCL communicator owned by the C-ABI (tcsl_cuda_nccl_comm_init) for the
+    row-sharded all-gather of Y. The unique id travels over the
+    caller's torch.distributed group (any backend)."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        torch = _torch()
+        L = lib()
+        if not L.tcsl_cuda_nccl_available():
+            raise TcslError(65, "libnccl.so.2 not found")
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            _check(L.tcsl_cuda_nccl_unique_id(C.c_void_p(uid.data_ptr())), "nccl id")
+        if world > 1:
+            backend = dist.get_backend(group)
+            t = uid.cuda() if backend == "nccl" else uid
+            dist.broadcast(t, 0, group=group)
+            uid = t.cpu()
+        self.comm = C.c_void_p()
+        _check(L.tcsl_cuda_nccl_comm_init(C.byref(self.comm), world, C.c_void_p(uid.data_ptr()), rank), "nccl init")
+        self.rank, self.world = rank, world
+
+    def allgather_rows(self, y_local, y_full):
+        """y_full[world * rows, n] = concat over ranks of y_local[rows, n] (fp32 or fp16)."""
+        torch = _torch()
+        f16 = y_local.dtype == torch.float16
+        rows, n = y_local.shape
+        _check(lib().tcsl_cuda_allgather_rows(_ptr(y_local), _ptr(y_full), rows, n, int(f16), self.comm, _stream()),
+               "allgather")
+        return y_full
+
+    def close(self):
+        if self.comm:
+            lib().tcsl_cuda_nccl_comm_destroy(self.comm)
+            self.comm = C.c_void_p()

@@ -1,5 +1,7 @@
 // The extern "C" boundary (include/tcsl_cuda.h): argument checks with the
 // reference's error classes, workspace carving, and kernel dispatch.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -48,10 +50,13 @@ int planned_split(uint32_t m, uint32_t k, int n, int split) {
 
 int effective_split(uint32_t m, uint32_t k, int n, int split_k) {
   if (split_k > 0) return planned_split(m, k, n, split_k);
-  // the heuristic simulates the persistent schedule; memoise it per shape
+  // the heuristic simulates the persistent schedule (SM count of the current
+  // device); memoise it per device and shape
   static std::mutex mu;
-  static std::map<std::tuple<uint32_t, uint32_t, int>, int> cache;
-  const auto key = std::make_tuple(m, k, n);
+  static std::map<std::tuple<int, uint32_t, uint32_t, int>, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) cudaGetLastError();
+  const auto key = std::make_tuple(dev, m, k, n);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
@@ -159,6 +164,147 @@ int tcsl_cuda_validate(const uint32_t* dOffsets, uint64_t n_entries, uint32_t m,
                                             static_cast<cudaStream_t>(stream)));
 }
 
+int tcsl_cuda_validate_entries(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m,
+                               uint32_t k, int m_tb, int k_tb, int mode, uint32_t* dFlags, int* dErr, void* stream) {
+  if (!tile_ok(m_tb, k_tb) || m == 0 || k == 0 || !dOffsets || (n_entries && !dEntries)) return TCSL_STATUS_INVALID_ARGUMENT;
+  if (mode < TCSL_CHECK_SPMM || mode > TCSL_CHECK_INGEST) return TCSL_STATUS_INVALID_ARGUMENT;
+  return cuda_status(tcslk::launch_validate_entries(dOffsets, dEntries, n_entries, m, k, m_tb, k_tb, mode, dFlags,
+                                                    dErr, static_cast<cudaStream_t>(stream)));
+}
+
+// ------------------------------------------------------------------ ingest
+// deserialize_tcsl (proj/src/tcsl_format.cpp:180-222): header fields and their
+// checks in the reference's order.
+int tcsl_cuda_parse_header(const void* bytes, size_t size, tcsl_cuda_header* out) {
+  if (!out || (!bytes && size)) return TCSL_STATUS_INVALID_ARGUMENT;
+  const uint8_t* p = static_cast<const uint8_t*>(bytes);
+  size_t at = 0;
+  auto le = [&](int nb, uint32_t* v) {
+    if (size - at < static_cast<size_t>(nb)) return false;
+    *v = 0;
+    for (int i = 0; i < nb; ++i) *v |= static_cast<uint32_t>(p[at + i]) << (8 * i);
+    at += nb;
+    return true;
+  };
+  constexpr int kTruncated = 5, kBadMagic = 1, kBadVersion = 2, kBadHeader = 3, kTrailing = 6;
+  if (size < 4) return kTruncated;
+  if (std::memcmp(p, "TCSL", 4) != 0) return kBadMagic;
+  at = 4;
+  uint32_t version = 0, flags = 0, m = 0, k = 0, m_tb = 0, k_tb = 0, nt = 0;
+  if (!le(2, &version)) return kTruncated;
+  if (version != 1) return kBadVersion;
+  if (!le(2, &flags)) return kTruncated;
+  if (flags & ~1u) return kBadVersion;
+  if (!le(4, &m) || !le(4, &k) || !le(4, &m_tb) || !le(4, &k_tb)) return kTruncated;
+  if (m == 0 || k == 0) return kBadHeader;
+  if (m_tb == 0 || k_tb == 0 || m_tb > 65536 || k_tb > 65536) return kBadHeader;
+  if (!tile_ok(static_cast<int>(m_tb), static_cast<int>(k_tb))) return kBadHeader;
+  if (!le(4, &nt)) return kTruncated;
+  const uint64_t want_tiles = static_cast<uint64_t>(tcslk::div_up_i(m, m_tb)) * tcslk::div_up_i(k, k_tb);
+  if (nt != want_tiles) return kBadHeader;
+  const size_t off_bytes = 4 * (static_cast<size_t>(nt) + 1);
+  if (size - at < off_bytes) return kTruncated;
+  uint32_t last = 0;
+  std::memcpy(&last, p + at + off_bytes - 4, 4);
+  const size_t payload = size - at - off_bytes;
+  if (payload != 4 * static_cast<size_t>(last)) {
+    // The reference checks the offset table before the payload size: report
+    // inconsistent_offsets when the table itself is malformed (host scan, error path only).
+    uint32_t prev = 0;
+    for (uint32_t i = 0; i <= nt; ++i) {
+      uint32_t o = 0;
+      std::memcpy(&o, p + at + 4 * static_cast<size_t>(i), 4);
+      if ((i == 0 && o != 0) || (i > 0 && (o < prev || ((o - prev) & 31u)))) return TCSL_STATUS_INCONSISTENT_OFFSETS;
+      prev = o;
+    }
+    return payload < 4 * static_cast<size_t>(last) ? kTruncated : kTrailing;
+  }
+  out->m = m;
+  out->k = k;
+  out->m_tb = m_tb;
+  out->k_tb = k_tb;
+  out->num_tiles = nt;
+  out->reordered = flags & 1u;
+  out->n_entries = last;
+  return TCSL_STATUS_OK;
+}
+
+int tcsl_cuda_ingest(const void* bytes, size_t size, const tcsl_cuda_header* h, uint32_t* dOffsets,
+                     uint32_t* dEntries, void* staging, size_t staging_bytes, uint32_t* dFlags, int* dErr,
+                     void* stream) {
+  if (!bytes || !h || !dOffsets || (h->n_entries && !dEntries)) return TCSL_STATUS_INVALID_ARGUMENT;
+  if (staging && staging_bytes < (1u << 20)) return TCSL_STATUS_INVALID_ARGUMENT;
+  const size_t off_bytes = 4 * (static_cast<size_t>(h->num_tiles) + 1), ent_bytes = 4 * h->n_entries;
+  if (size != 28 + off_bytes + ent_bytes) return TCSL_STATUS_INVALID_ARGUMENT;  // parse_header first
+  auto s = static_cast<cudaStream_t>(stream);
+  const uint8_t* src = static_cast<const uint8_t*>(bytes) + 28;
+  cudaError_t e = cudaSuccess;
+  if (!staging) {  // caller's buffer is pinned (or accepts a synchronous pageable copy)
+    e = cudaMemcpyAsync(dOffsets, src, off_bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && ent_bytes)
+      e = cudaMemcpyAsync(dEntries, src + off_bytes, ent_bytes, cudaMemcpyHostToDevice, s);
+  } else {
+    // pageable source: two pinned halves, host memcpy of chunk i+1 overlaps the DMA of chunk i
+    const size_t half = (staging_bytes / 2) & ~size_t(255);
+    cudaEvent_t ev[2];
+    bool ev_ok[2] = {false, false};
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+      ev_ok[i] = e == cudaSuccess;
+    }
+    struct Part {
+      uint8_t* dst;
+      const uint8_t* src;
+      size_t n;
+    } parts[2] = {{reinterpret_cast<uint8_t*>(dOffsets), src, off_bytes},
+                  {reinterpret_cast<uint8_t*>(dEntries), src + off_bytes, ent_bytes}};
+    int slot = 0;
+    bool used[2] = {false, false};
+    for (const Part& part : parts) {
+      for (size_t pos = 0; pos < part.n && e == cudaSuccess; pos += half, slot ^= 1) {
+        const size_t c = std::min(half, part.n - pos);
+        uint8_t* buf = static_cast<uint8_t*>(staging) + slot * half;
+        if (used[slot]) e = cudaEventSynchronize(ev[slot]);
+        if (e != cudaSuccess) break;
+        std::memcpy(buf, part.src + pos, c);
+        e = cudaMemcpyAsync(part.dst + pos, buf, c, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[slot], s);
+        used[slot] = true;
+      }
+    }
+    for (int i = 0; i < 2; ++i) {
+      if (ev_ok[i] && used[i]) {
+        const cudaError_t e2 = cudaEventSynchronize(ev[i]);
+        if (e == cudaSuccess) e = e2;
+      }
+      if (ev_ok[i]) cudaEventDestroy(ev[i]);
+    }
+  }
+  if (e != cudaSuccess) return cuda_status(e);
+  return cuda_status(tcslk::launch_validate_entries(dOffsets, dEntries, h->n_entries, h->m, h->k,
+                                                    static_cast<int>(h->m_tb), static_cast<int>(h->k_tb),
+                                                    TCSL_CHECK_INGEST, dFlags, dErr, s));
+}
+
+// -------------------------------------------------------------------- prune
+int tcsl_cuda_prune_workspace(uint64_t count, size_t* ws_bytes) {
+  if (!ws_bytes) return TCSL_STATUS_INVALID_ARGUMENT;
+  *ws_bytes = tcslk::prune_workspace_bytes(count);
+  return TCSL_STATUS_OK;
+}
+
+int tcsl_cuda_prune_magnitude(const uint16_t* dA, uint64_t count, double beta, uint16_t* dOut, void* ws,
+                              size_t ws_bytes, void* stream) {
+  // matrix.cpp:69-75: beta in [0, 1], cut = floor(beta * n) clamped to [0, n]
+  if (!(beta >= 0.0 && beta <= 1.0)) return TCSL_STATUS_INVALID_ARGUMENT;
+  if (count && (!dA || !dOut)) return TCSL_STATUS_INVALID_ARGUMENT;
+  if (!ws || ws_bytes < tcslk::prune_workspace_bytes(count)) return TCSL_STATUS_WORKSPACE;
+  long long cut = static_cast<long long>(std::floor(beta * static_cast<double>(count)));
+  cut = std::max(0ll, std::min(cut, static_cast<long long>(count)));
+  return cuda_status(tcslk::launch_prune(dA, count, static_cast<uint64_t>(cut), dOut, ws, ws_bytes,
+                                         static_cast<cudaStream_t>(stream)));
+}
+
 // -------------------------------------------------------------------- spmm
 int tcsl_cuda_spmm_auto_split(uint32_t m, uint32_t k, int n) { return effective_split(m, k, n, 0); }
 
@@ -169,8 +315,17 @@ int tcsl_cuda_spmm_exact_workspace(uint32_t m, uint32_t k, size_t* ws_bytes) {
 }
 
 int tcsl_cuda_spmm_workspace(uint32_t m, uint32_t k, int m_tb, int k_tb, int n, int split_k, size_t* ws_bytes) {
-  if (!tile_ok(m_tb, k_tb) || n <= 0 || !ws_bytes) return TCSL_STATUS_INVALID_ARGUMENT;
-  if (!is_default_tile(m_tb, k_tb)) return tcsl_cuda_spmm_exact_workspace(m, k, ws_bytes);
+  return tcsl_cuda_spmm_ex_workspace(m, k, m_tb, k_tb, n, split_k, 0, ws_bytes);
+}
+
+int tcsl_cuda_spmm_ex_workspace(uint32_t m, uint32_t k, int m_tb, int k_tb, int n, int split_k, int exact,
+                                size_t* ws_bytes) {
+  if (!tile_ok(m_tb, k_tb) || n <= 0 || split_k < 0 || !ws_bytes) return TCSL_STATUS_INVALID_ARGUMENT;
+  if (exact || !is_default_tile(m_tb, k_tb)) {
+    // dense reconstruction + an fp32 staging buffer for the fused epilogue
+    *ws_bytes = align256(static_cast<size_t>(m) * k * 2) + align256(static_cast<size_t>(m) * n * 4);
+    return TCSL_STATUS_OK;
+  }
   *ws_bytes = spmm_ws_layout(m, k, n, effective_split(m, k, n, split_k), true).total;
   return TCSL_STATUS_OK;
 }
@@ -178,35 +333,49 @@ int tcsl_cuda_spmm_workspace(uint32_t m, uint32_t k, int m_tb, int k_tb, int n, 
 int tcsl_cuda_spmm_exact(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m,
                          uint32_t k, int m_tb, int k_tb, const uint16_t* dX, int n, float* dY, void* ws,
                          size_t ws_bytes, int* dErr, void* stream) {
-  // engine.cpp:28-32
-  if (!tile_ok(m_tb, k_tb) || n <= 0 || m == 0 || k == 0) return TCSL_STATUS_INVALID_ARGUMENT;
-  if (!dOffsets || !dX || !dY) return TCSL_STATUS_INVALID_ARGUMENT;
-  size_t need = 0;
-  tcsl_cuda_spmm_exact_workspace(m, k, &need);
-  if (!ws || ws_bytes < need) return TCSL_STATUS_WORKSPACE;
-  auto s = static_cast<cudaStream_t>(stream);
-  uint16_t* dense = static_cast<uint16_t*>(ws);
-  cudaError_t e = tcslk::launch_decode(dOffsets, dEntries, n_entries, m, k, m_tb, k_tb, dense, dErr, 0, s);
-  if (e == cudaSuccess) e = tcslk::launch_dense_gemm_exact(dense, m, k, dX, n, dY, s);
-  return cuda_status(e);
+  return tcsl_cuda_spmm_ex(dOffsets, dEntries, n_entries, m, k, m_tb, k_tb, dX, n, dY, TCSL_OUT_F32, nullptr,
+                           TCSL_ACT_NONE, 0, 1, ws, ws_bytes, dErr, stream);
 }
 
 int tcsl_cuda_spmm(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m, uint32_t k,
                    int m_tb, int k_tb, const uint16_t* dX, int n, float* dY, int split_k, void* ws,
                    size_t ws_bytes, int* dErr, void* stream) {
+  return tcsl_cuda_spmm_ex(dOffsets, dEntries, n_entries, m, k, m_tb, k_tb, dX, n, dY, TCSL_OUT_F32, nullptr,
+                           TCSL_ACT_NONE, split_k, 0, ws, ws_bytes, dErr, stream);
+}
+
+int tcsl_cuda_spmm_ex(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m,
+                      uint32_t k, int m_tb, int k_tb, const uint16_t* dX, int n, void* dY, int out_dtype,
+                      const float* dBias, int activation, int split_k, int exact, void* ws, size_t ws_bytes,
+                      int* dErr, void* stream) {
+  // engine.cpp:28-32 (the dimension check is the caller's: no B shape crosses the ABI)
   if (!tile_ok(m_tb, k_tb) || n <= 0 || m == 0 || k == 0 || split_k < 0) return TCSL_STATUS_INVALID_ARGUMENT;
+  if (out_dtype != TCSL_OUT_F32 && out_dtype != TCSL_OUT_F16) return TCSL_STATUS_INVALID_ARGUMENT;
+  if (activation < TCSL_ACT_NONE || activation > TCSL_ACT_GELU_TANH) return TCSL_STATUS_INVALID_ARGUMENT;
   if (!dOffsets || !dX || !dY || (n_entries && !dEntries)) return TCSL_STATUS_INVALID_ARGUMENT;
-  if (!is_default_tile(m_tb, k_tb))
-    return tcsl_cuda_spmm_exact(dOffsets, dEntries, n_entries, m, k, m_tb, k_tb, dX, n, dY, ws, ws_bytes, dErr,
-                                stream);
   auto s = static_cast<cudaStream_t>(stream);
+  const bool fused = dBias != nullptr || activation != TCSL_ACT_NONE || out_dtype == TCSL_OUT_F16;
+  float* y32 = out_dtype == TCSL_OUT_F32 ? static_cast<float*>(dY) : nullptr;
+  uint16_t* y16 = out_dtype == TCSL_OUT_F16 ? static_cast<uint16_t*>(dY) : nullptr;
+  cudaError_t e = cudaSuccess;
+  if (exact || !is_default_tile(m_tb, k_tb)) {
+    const size_t need = align256(static_cast<size_t>(m) * k * 2) + (fused ? align256(static_cast<size_t>(m) * n * 4) : 0);
+    if (!ws || ws_bytes < need) return TCSL_STATUS_WORKSPACE;
+    uint16_t* dense = static_cast<uint16_t*>(ws);
+    float* tmp = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(static_cast<size_t>(m) * k * 2));
+    e = tcslk::launch_decode(dOffsets, dEntries, n_entries, m, k, m_tb, k_tb, dense, dErr, 0, s);
+    if (e == cudaSuccess) e = tcslk::launch_dense_gemm_exact(dense, m, k, dX, n, fused ? tmp : y32, s);
+    if (e == cudaSuccess && fused) e = tcslk::launch_reduce_epilogue(tmp, 1, m, n, dBias, activation, y32, y16, s);
+    return cuda_status(e);
+  }
+  // cp.async.bulk streams 128-B spans of the entries: they must be 16-B aligned
+  if (reinterpret_cast<uintptr_t>(dEntries) & 15u) return TCSL_STATUS_INVALID_ARGUMENT;
   const int split = effective_split(m, k, n, split_k);
   const bool pad_x = (n % 8) != 0 || (reinterpret_cast<uintptr_t>(dX) & 15u) != 0;
   const SpmmWs lay = spmm_ws_layout(m, k, n, split, pad_x);
   if (lay.total && (!ws || ws_bytes < lay.total)) return TCSL_STATUS_WORKSPACE;
   const uint16_t* x = dX;
   int ldx = n;
-  cudaError_t e = cudaSuccess;
   if (pad_x) {
     uint16_t* xp = static_cast<uint16_t*>(ws);
     ldx = x_pitch(n);
@@ -219,9 +388,19 @@ int tcsl_cuda_spmm(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t 
   }
   tcslk::SpmmPlan plan;
   tcslk::spmm_sm100_plan(m, k, n, split, &plan);
-  float* out = split > 1 ? reinterpret_cast<float*>(static_cast<char*>(ws) + lay.x_pad) : dY;
-  e = tcslk::launch_spmm_sm100(plan, dOffsets, dEntries, n_entries, m, k, x, ldx, out, dErr, s);
-  if (e == cudaSuccess && split > 1) e = tcslk::launch_splitk_reduce(out, split, static_cast<size_t>(m) * n, dY, s);
+  if (split > 1) {
+    float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + lay.x_pad);
+    e = tcslk::launch_spmm_sm100(plan, dOffsets, dEntries, n_entries, m, k, x, ldx, part, dErr, s);
+    if (e == cudaSuccess)
+      e = fused ? tcslk::launch_reduce_epilogue(part, split, m, n, dBias, activation, y32, y16, s)
+                : tcslk::launch_splitk_reduce(part, split, static_cast<size_t>(m) * n, y32, s);
+  } else {
+    tcslk::Epilogue epi;
+    epi.bias = dBias;
+    epi.act = activation;
+    epi.out16 = y16;
+    e = tcslk::launch_spmm_sm100(plan, dOffsets, dEntries, n_entries, m, k, x, ldx, y32, dErr, s, epi);
+  }
   return cuda_status(e);
 }
 

@@ -13,39 +13,75 @@ namespace tcslk {
 
 namespace {
 
+// One block per tile; `strict` is a TCSL_CHECK_* mode. DECODE: decode's rules (tcsl_format.cpp:126-155 after
+// check_offsets :19-32): whole 32-entry groups, first offset 0, last == E, and a
+// nonzero value in the padded fringe is location_out_of_range. INGEST:
+// deserialize_tcsl's rules (check_offsets only; entry problems become flags). SPMM:
+// extract_tile's rules as spmm uses them (engine.cpp:8-25): only the tile's own
+// span is checked and fringe entries are dropped. A location repeated inside a
+// tile is detected with a bitmap (tile_elems <= 65536 bits = 8 KB of smem); such
+// a tile is rewritten serially in entry order so the last entry wins, as in the
+// reference's sequential loops. out == nullptr: validation only.
 __global__ void decode_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ ent,
                               uint64_t n_entries, uint32_t m, uint32_t k, int m_tb, int k_tb, int tiles_k,
-                              uint32_t tiles, uint16_t* __restrict__ out, int* err, int strict) {
+                              uint32_t tiles, uint16_t* __restrict__ out, int* err, int strict,
+                              uint32_t* flags) {
+  extern __shared__ uint32_t seen[];
   const uint32_t tile = blockIdx.x;
   const uint32_t a = off[tile], b = off[tile + 1];
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && strict) {
     if (tile == 0 && a != 0) raise_dev(err, TCSL_STATUS_INCONSISTENT_OFFSETS);
     if (tile + 1 == tiles && b != n_entries) raise_dev(err, TCSL_STATUS_INCONSISTENT_OFFSETS);
   }
-  if (b < a || b > n_entries || ((b - a) & 31u)) {
+  if (b < a || b > n_entries || (strict && ((b - a) & 31u))) {
     if (threadIdx.x == 0) raise_dev(err, TCSL_STATUS_INCONSISTENT_OFFSETS);
     return;
   }
+  if (threadIdx.x == 0 && flags && (((b - a) & 31u) || (a & 31u))) atomicOr(flags, kFlagPartialGroups);
   const long long r0 = static_cast<long long>(tile / tiles_k) * m_tb;
   const long long c0 = static_cast<long long>(tile % tiles_k) * k_tb;
   const uint32_t elems = static_cast<uint32_t>(m_tb) * k_tb;
+  for (uint32_t w = threadIdx.x; w < (elems + 31) / 32; w += blockDim.x) seen[w] = 0;
+  __syncthreads();
+  bool dup = false, fringe = false, range = false;
   for (uint32_t e = a + threadIdx.x; e < b; e += blockDim.x) {
     const uint32_t v = ent[e];
     const uint32_t loc = v & 0xFFFFu;
     if (loc >= elems) {
-      raise_dev(err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
+      range = true;
+      if (strict != TCSL_CHECK_INGEST) raise_dev(err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
       continue;
     }
+    const uint32_t bit = 1u << (loc & 31u);
+    dup |= (atomicOr(&seen[loc >> 5], bit) & bit) != 0;
     const long long r = r0 + loc / k_tb, c = c0 + loc % k_tb;
     uint16_t val = static_cast<uint16_t>(v >> 16);
     if ((val & 0x7FFFu) == 0) val = 0;  // -0 -> +0 (half.hpp:27)
     if (r >= m || c >= k) {
       // decode rejects fringe payloads (tcsl_format.cpp:146-149); spmm's extract_tile
       // (engine.cpp:8-25) lets them through and the crop / zero-padded B removes them.
-      if (val && strict) raise_dev(err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
+      if (val) {
+        fringe = true;
+        if (strict == TCSL_CHECK_DECODE) raise_dev(err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
+      }
       continue;
     }
-    out[r * k + c] = val;
+    if (out) out[r * k + c] = val;
+  }
+  if (__syncthreads_or(fringe) && flags && threadIdx.x == 0) atomicOr(flags, kFlagFringePayload);
+  if (__syncthreads_or(range) && flags && threadIdx.x == 0) atomicOr(flags, TCSL_FLAG_LOCATION_RANGE);
+  if (__syncthreads_or(dup) && threadIdx.x == 0) {
+    if (flags) atomicOr(flags, kFlagDuplicates);
+    for (uint32_t e = a; e < b && out; ++e) {  // sequential replay: the last entry wins
+      const uint32_t v = ent[e];
+      const uint32_t loc = v & 0xFFFFu;
+      if (loc >= elems) continue;
+      const long long r = r0 + loc / k_tb, c = c0 + loc % k_tb;
+      if (r >= m || c >= k) continue;
+      uint16_t val = static_cast<uint16_t>(v >> 16);
+      if ((val & 0x7FFFu) == 0) val = 0;
+      out[r * k + c] = val;
+    }
   }
 }
 
@@ -118,6 +154,23 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ p, int split, siz
   }
 }
 
+// Split-K sum in ascending s (as splitk_reduce_kernel) followed by the fused
+// epilogue of tcsl_cuda_spmm_ex; split == 1 is a pure epilogue pass.
+__global__ void reduce_epilogue_kernel(const float* __restrict__ p, int split, size_t count, int n,
+                                       const float* __restrict__ bias, int act, float* __restrict__ y32,
+                                       uint16_t* __restrict__ y16) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+    float acc = p[i];
+    for (int s = 1; s < split; ++s) acc = __fadd_rn(acc, p[static_cast<size_t>(s) * count + i]);
+    const float v = epilogue_value(acc, bias ? __ldg(bias + i / static_cast<size_t>(n)) : 0.0f, act);
+    if (y16)
+      y16[i] = static_cast<uint16_t>(f16_bits_rne(v));
+    else
+      y32[i] = v;
+  }
+}
+
 __global__ void rebase_kernel(const uint32_t* __restrict__ off, uint32_t t0, uint32_t n,
                               uint32_t* __restrict__ out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -156,7 +209,22 @@ cudaError_t launch_decode(const uint32_t* off, const uint32_t* ent, uint64_t n_e
   const uint32_t tiles = static_cast<uint32_t>(div_up_i(m, m_tb)) * tk;
   cudaError_t e = cudaMemsetAsync(out, 0, static_cast<size_t>(m) * k * 2, s);
   if (e != cudaSuccess) return e;
-  if (tiles) decode_kernel<<<tiles, 256, 0, s>>>(off, ent, n_entries, m, k, m_tb, k_tb, tk, tiles, out, err, strict);
+  const size_t smem = 4 * ((static_cast<size_t>(m_tb) * k_tb + 31) / 32);
+  if (tiles)
+    decode_kernel<<<tiles, 256, smem, s>>>(off, ent, n_entries, m, k, m_tb, k_tb, tk, tiles, out, err, strict,
+                                           nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate_entries(const uint32_t* off, const uint32_t* ent, uint64_t n_entries, uint32_t m,
+                                    uint32_t k, int m_tb, int k_tb, int strict, uint32_t* flags, int* err,
+                                    cudaStream_t s) {
+  const int tk = div_up_i(k, k_tb);
+  const uint32_t tiles = static_cast<uint32_t>(div_up_i(m, m_tb)) * tk;
+  const size_t smem = 4 * ((static_cast<size_t>(m_tb) * k_tb + 31) / 32);
+  if (tiles)
+    decode_kernel<<<tiles, 256, smem, s>>>(off, ent, n_entries, m, k, m_tb, k_tb, tk, tiles, nullptr, err, strict,
+                                           flags);
   return cudaGetLastError();
 }
 
@@ -178,6 +246,15 @@ cudaError_t launch_splitk_reduce(const float* p, int split, size_t count, float*
   const size_t work = (count & 3u) == 0 ? count / 4 : count;
   const int blocks = static_cast<int>(std::min<size_t>((work + 255) / 256, 148 * 8));
   splitk_reduce_kernel<<<blocks, 256, 0, s>>>(p, split, count, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_epilogue(const float* p, int split, uint32_t m, int n, const float* bias, int act,
+                                   float* y32, uint16_t* y16, cudaStream_t s) {
+  const size_t count = static_cast<size_t>(m) * n;
+  if (count == 0) return cudaSuccess;
+  const int blocks = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 8));
+  reduce_epilogue_kernel<<<blocks, 256, 0, s>>>(p, split, count, n, bias, act, y32, y16);
   return cudaGetLastError();
 }
 

@@ -49,6 +49,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <vector>
 
@@ -178,7 +179,11 @@ struct Params {
   uint32_t m, k;
   int tiles_m, tiles_k, tiles_mp;
   int n, col0, split, units;
-  float* out;
+  float* out;       // fp32 Y or split-K partials (out_f16 == 0)
+  uint16_t* out16;  // binary16 Y (out_f16 == 1, split == 1)
+  const float* bias;  // per-row bias (split == 1) or nullptr
+  int act;            // TCSL_ACT_* (split == 1)
+  int out_f16;
   int ldo;
   int* err;
   unsigned long long* trace;  // TCSL_TRACE builds only: per-event clock64 stamps of CTA 0
@@ -601,12 +606,37 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
         const bool row_ok = row < p.m;
         const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * C::kN;
         const int ncol = min(C::kN, p.n - p.col0);
+        const bool fused = p.bias != nullptr || p.act != 0 || p.out_f16;  // split == 1 only (host)
+        const float b_row = (p.bias != nullptr && row_ok) ? __ldg(p.bias + row) : 0.0f;
 #pragma unroll
         for (int c0 = 0; c0 < C::kN; c0 += 16) {
           uint32_t r[16];
           tmem_ld16(t_base + c0, r);
           tmem_ld_wait();
-          if (row_ok) {
+          if (row_ok && fused) {
+            // fused epilogue: act(acc + bias) in fp32, optionally narrowed RNE to binary16
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = epilogue_value(__uint_as_float(r[j]), b_row, p.act);
+            if (p.out_f16) {
+              uint16_t* d16 = p.out16 + row * p.ldo + p.col0 + c0;
+              if (c0 + 16 <= ncol && ((reinterpret_cast<uintptr_t>(d16) & 15u) == 0)) {
+                uint32_t h[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) h[j] = f16_bits_rne(v[2 * j]) | (f16_bits_rne(v[2 * j + 1]) << 16);
+                reinterpret_cast<uint4*>(d16)[0] = make_uint4(h[0], h[1], h[2], h[3]);
+                reinterpret_cast<uint4*>(d16)[1] = make_uint4(h[4], h[5], h[6], h[7]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (c0 + j < ncol) d16[j] = static_cast<uint16_t>(f16_bits_rne(v[j]));
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (c0 + j < ncol) dst[c0 + j] = v[j];
+            }
+          } else if (row_ok) {
             if (c0 + 16 <= ncol && ((reinterpret_cast<uintptr_t>(dst + c0) & 15u) == 0)) {
               float4* d4 = reinterpret_cast<float4*>(dst + c0);
 #pragma unroll
@@ -938,13 +968,30 @@ int half_n(int n) {
   return 128;
 }
 
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    cudaGetLastError();
+    dev = 0;
+  }
+  return dev;
+}
+
+// Per device (the smem attribute and the occupancy are per-device properties):
+// the >48 KB dynamic-smem opt-in and the co-resident cluster count. Returns 0
+// with *e set when the attribute cannot be applied.
 template <int NH, class TM>
-int max_clusters() {
-  static int cached = 0;
+int max_clusters(cudaError_t* e) {
+  static std::atomic<int> cache[kMaxDevices];
+  const int dev = current_device();
+  int cached = cache[dev].load(std::memory_order_acquire);
   if (!cached) {
     using C = Cfg<NH, TM::kNA>;
-    cudaFuncSetAttribute(spmm_sm100_kernel<NH, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(C::kSmem));
+    *e = cudaFuncSetAttribute(spmm_sm100_kernel<NH, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(C::kSmem));
+    if (*e != cudaSuccess) return 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * 74, 1, 1);
     cfg.blockDim = dim3(TM::kThreads, 1, 1);
@@ -962,6 +1009,7 @@ int max_clusters() {
       nc = num_sms() / 2;
     }
     cached = nc;
+    cache[dev].store(nc, std::memory_order_release);
   }
   return cached;
 }
@@ -988,7 +1036,10 @@ template <int NH, class TM>
 cudaError_t launch_shape(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
   using C = Cfg<NH, TM::kNA>;
   static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
-  const int nc = std::min(clusters, max_clusters<NH, TM>());
+  cudaError_t e = cudaSuccess;
+  const int mc = max_clusters<NH, TM>(&e);
+  if (e != cudaSuccess) return e;
+  const int nc = std::min(clusters, mc);
   if ((p.units + nc - 1) / nc > kMaxUnits) return cudaErrorInvalidConfiguration;  // unit table size
   spmm_sm100_kernel<NH, TM><<<2 * nc, TM::kThreads, C::kSmem, s>>>(tm, p);
   return cudaGetLastError();
@@ -1021,14 +1072,15 @@ cudaError_t launch_nh(const Params& p, const CUtensorMap& tm, int clusters, cuda
 unsigned long long* g_trace = nullptr;
 
 int num_sms() {
-  static int sms = 0;
+  static std::atomic<int> cache[kMaxDevices];
+  const int dev = current_device();
+  int sms = cache[dev].load(std::memory_order_acquire);
   if (!sms) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
       cudaGetLastError();
       sms = 148;
     }
+    cache[dev].store(sms, std::memory_order_release);
   }
   return sms;
 }
@@ -1073,7 +1125,7 @@ int spmm_sm100_plan(uint32_t m, uint32_t k, int n, int split_k, SpmmPlan* plan) 
 
 cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const uint32_t* ent,
                               uint64_t n_entries, uint32_t m, uint32_t k, const uint16_t* x, int ldx,
-                              float* out, int* err, cudaStream_t s) {
+                              float* out, int* err, cudaStream_t s, const Epilogue& epi) {
   auto encode = tensor_map_encoder();
   if (!encode) return cudaErrorNotSupported;
   Params p{};
@@ -1089,6 +1141,10 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
   p.split = plan.split;
   p.units = plan.units;
   p.out = out;
+  p.out16 = epi.out16;
+  p.out_f16 = epi.out16 != nullptr;
+  p.bias = epi.bias;
+  p.act = epi.act;
   p.ldo = plan.n;
   p.err = err;
   p.trace = g_trace;

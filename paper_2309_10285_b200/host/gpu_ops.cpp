@@ -5,6 +5,7 @@
 //   decode        proj/src/tcsl_format.cpp:126-155  -> tcsl_cuda_decode
 //   spmm          proj/src/engine.cpp:27-78         -> tcsl_cuda_spmm / _exact
 //   dense_gemm_ref proj/src/gemm.cpp:7-44           -> tcsl_cuda_spmm_exact on encode(A)
+//   prune_magnitude proj/src/matrix.cpp:69-100      -> tcsl_cuda_prune_magnitude (radix select)
 //   extract_tile, reg_pressure (engine.cpp:8-25, 80-91) stay on the host (O(entries of a tile)).
 #include <algorithm>
 #include <cstring>
@@ -47,7 +48,7 @@ class DeviceSlot {
 };
 
 struct Scratch {
-  DeviceSlot dense, offsets, entries, x, y, ws, err;
+  DeviceSlot dense, offsets, entries, x, y, ws, err, flags;
 };
 
 Scratch& scratch() {
@@ -81,16 +82,6 @@ const std::uint16_t* upload_half(DeviceSlot& slot, const HalfMatrix& a) {
   auto* d = static_cast<std::uint16_t*>(slot.get(2 * std::max<std::size_t>(static_cast<std::size_t>(a.size()), 1)));
   check(tcsl_cuda_memcpy_h2d(d, a.data(), 2 * static_cast<std::size_t>(a.size()), nullptr), "upload");
   return d;
-}
-
-// spmm only checks each tile's own span (engine.cpp:8-14): spans that are not
-// whole 32-entry groups are legal for the reference but not for the grouped
-// GPU decoders, so those inputs take the bit-exact element-wise path instead.
-bool whole_groups(const TcslMatrix& t) {
-  for (std::size_t i = 0; i + 1 < t.tile_offsets.size(); ++i)
-    if (t.tile_offsets[i + 1] < t.tile_offsets[i] || (t.tile_offsets[i + 1] - t.tile_offsets[i]) % kGroupSize)
-      return false;
-  return !t.tile_offsets.empty() && t.tile_offsets[0] == 0 && t.tile_offsets.back() == t.entries.size();
 }
 
 }  // namespace
@@ -172,30 +163,35 @@ FloatMatrix spmm(const TcslMatrix& a, const HalfMatrix& b, const SpmmOptions& op
       raise(Errc::inconsistent_offsets, "offset table does not match entries");
   const int n = static_cast<int>(b.cols());
   FloatMatrix c(a.m, n);
-  if (!whole_groups(a)) {  // lenient spans: element-wise, bit-exact host reconstruction on the GPU path
-    HalfMatrix dense(a.m, a.k);
-    dense.setZero();
-    for (std::uint32_t t = 0; t < a.num_tiles(); ++t) {
-      const std::vector<HalfBits> tile = extract_tile(a, t);
-      const int r0 = static_cast<int>(t) / a.tiles_k() * a.cfg.m_tb, c0 = static_cast<int>(t) % a.tiles_k() * a.cfg.k_tb;
-      for (int x = 0; x < a.cfg.m_tb && r0 + x < static_cast<int>(a.m); ++x)
-        for (int y = 0; y < a.cfg.k_tb && c0 + y < static_cast<int>(a.k); ++y)
-          dense(r0 + x, c0 + y) = half_from_bits(tile[static_cast<std::size_t>(x) * a.cfg.k_tb + y]);
-    }
-    return dense_gemm_ref(dense, b, a.cfg);
-  }
   const DeviceTcsl d = upload(a);
   Scratch& s = scratch();
+  // The reference accepts tiles whose spans are not whole 32-entry groups and
+  // locations repeated inside a tile (last writer wins, engine.cpp:8-25); the
+  // tensor-core decoders need neither. One device pass over the uploaded entries
+  // finds out, and such matrices take the bit-exact path, which handles both.
+  bool exact = opt.exact;
+  if (!exact && a.cfg.m_tb == 128 && a.cfg.k_tb == 64) {
+    auto* flags = static_cast<std::uint32_t*>(s.flags.get(sizeof(std::uint32_t)));
+    check(tcsl_cuda_memset(flags, 0, sizeof(std::uint32_t), nullptr), "memset");
+    int* verr = fresh_error_word();
+    check(tcsl_cuda_validate_entries(d.off, d.ent, a.entries.size(), a.m, a.k, a.cfg.m_tb, a.cfg.k_tb, TCSL_CHECK_SPMM,
+                                     flags, verr, nullptr),
+          "spmm");
+    std::uint32_t h = 0;
+    check(tcsl_cuda_memcpy_d2h(&h, flags, sizeof h, nullptr), "spmm");
+    collect_errors(verr, "spmm");
+    exact = (h & (TCSL_FLAG_DUPLICATE_LOCATIONS | TCSL_FLAG_PARTIAL_GROUPS)) != 0;
+  }
   const std::uint16_t* x = upload_half(s.x, b);
   auto* y = static_cast<float*>(s.y.get(4ull * a.m * n));
   std::size_t ws_bytes = 0;
-  if (opt.exact)
+  if (exact)
     check(tcsl_cuda_spmm_exact_workspace(a.m, a.k, &ws_bytes), "spmm");
   else
     check(tcsl_cuda_spmm_workspace(a.m, a.k, a.cfg.m_tb, a.cfg.k_tb, n, opt.split_k, &ws_bytes), "spmm");
   void* ws = s.ws.get(std::max<std::size_t>(ws_bytes, 256));
   int* err = fresh_error_word();
-  if (opt.exact)
+  if (exact)
     check(tcsl_cuda_spmm_exact(d.off, d.ent, a.entries.size(), a.m, a.k, a.cfg.m_tb, a.cfg.k_tb, x, n, y, ws,
                                ws_bytes, err, nullptr),
           "spmm");
@@ -216,6 +212,23 @@ int reg_pressure(const TcslMatrix& t) {
   for (std::uint32_t tile = 0; tile < t.num_tiles(); ++tile)
     worst = std::max(worst, div_up(t.tile_entry_count(tile), t.cfg.threads_per_block));
   return worst;
+}
+
+HalfMatrix prune_magnitude(const HalfMatrix& a, double beta) {
+  if (!(beta >= 0.0 && beta <= 1.0)) raise(Errc::invalid_argument, "sparsity must be in [0, 1]");
+  HalfMatrix out = a;
+  const auto n = static_cast<std::uint64_t>(a.size());
+  if (n == 0) return out;
+  Scratch& s = scratch();
+  auto* d = static_cast<std::uint16_t*>(s.dense.get(2 * n));
+  check(tcsl_cuda_memcpy_h2d(d, a.data(), 2 * n, nullptr), "prune");
+  std::size_t ws_bytes = 0;
+  check(tcsl_cuda_prune_workspace(n, &ws_bytes), "prune");
+  void* ws = s.ws.get(ws_bytes);
+  check(tcsl_cuda_prune_magnitude(d, n, beta, d, ws, ws_bytes, nullptr), "prune");
+  check(tcsl_cuda_memcpy_d2h(out.data(), d, 2 * n, nullptr), "prune");
+  check(tcsl_cuda_stream_sync(nullptr), "prune");
+  return out;
 }
 
 FloatMatrix dense_gemm_ref(const HalfMatrix& a, const HalfMatrix& b, const TileConfig& cfg) {

@@ -1,5 +1,5 @@
 // Host-side pieces of the tcsl API that carry no device work: error names,
-// binary16 conversions, tile-config checks, synthetic inputs and pruning.
+// binary16 conversions, tile-config checks and synthetic inputs.
 // Behaviour follows proj/src/{errors,half,matrix}.cpp (cited per function).
 #include <algorithm>
 #include <cmath>
@@ -11,6 +11,7 @@
 #include "tcsl/errors.hpp"
 #include "tcsl/half.hpp"
 #include "tcsl/matrix.hpp"
+#include "tcsl_host.h"
 
 namespace tcsl {
 
@@ -60,18 +61,15 @@ int tile_n_for(int n) { return n <= 8 ? 8 : n <= 16 ? 16 : n <= 64 ? 32 : 64; } 
 // proj/src/matrix.cpp:35-67: one mt19937_64 draw decides zero/non-zero for
 // each position (selection sampling keeps the zero count exact); a second
 // draw builds a non-zero value.
-HalfMatrix gen_random_sparse(int rows, int cols, double beta, std::uint64_t seed) {
-  if (rows <= 0 || cols <= 0) raise(Errc::invalid_argument, "matrix dims must be positive");
-  if (!(beta >= 0.0 && beta <= 1.0)) raise(Errc::invalid_argument, "sparsity must be in [0, 1]");
-  const std::int64_t total = static_cast<std::int64_t>(rows) * cols;
+namespace {
+
+void gen_into(std::int64_t total, double beta, std::uint64_t seed, std::uint16_t* dst) {
   std::int64_t zeros_left = std::clamp<std::int64_t>(std::llround(beta * static_cast<double>(total)), 0, total);
-  HalfMatrix out(rows, cols);
   std::mt19937_64 rng(seed);
-  Eigen::half* dst = out.data();
   for (std::int64_t pos = 0; pos < total; ++pos) {
     const std::uint64_t unfilled = static_cast<std::uint64_t>(total - pos);
     if (rng() % unfilled < static_cast<std::uint64_t>(zeros_left)) {
-      dst[pos] = half_from_bits(kHalfPosZero);
+      dst[pos] = kHalfPosZero;
       --zeros_left;
       continue;
     }
@@ -79,31 +77,17 @@ HalfMatrix gen_random_sparse(int rows, int cols, double beta, std::uint64_t seed
     const HalfBits mantissa = static_cast<HalfBits>(bits & 0x3FFu);
     const HalfBits exponent = static_cast<HalfBits>(13u + (bits >> 10) % 5u);
     const HalfBits sign = static_cast<HalfBits>((bits >> 63) << 15);
-    dst[pos] = half_from_bits(static_cast<HalfBits>(sign | (exponent << 10) | mantissa));
+    dst[pos] = static_cast<HalfBits>(sign | (exponent << 10) | mantissa);
   }
-  return out;
 }
 
-// proj/src/matrix.cpp:69-100. The order (|v| ascending, NaN last, larger index
-// first among ties) is total, so a partial sort selects the same element set.
-HalfMatrix prune_magnitude(const HalfMatrix& a, double beta) {
+}  // namespace
+
+HalfMatrix gen_random_sparse(int rows, int cols, double beta, std::uint64_t seed) {
+  if (rows <= 0 || cols <= 0) raise(Errc::invalid_argument, "matrix dims must be positive");
   if (!(beta >= 0.0 && beta <= 1.0)) raise(Errc::invalid_argument, "sparsity must be in [0, 1]");
-  HalfMatrix out = a;
-  const std::int64_t total = a.size();
-  const std::int64_t cut = std::clamp<std::int64_t>(static_cast<std::int64_t>(std::floor(beta * total)), 0, total);
-  if (cut == 0) return out;
-  std::vector<float> mag(static_cast<std::size_t>(total));
-  for (std::int64_t i = 0; i < total; ++i) {
-    const float m = std::fabs(f32_from_f16(bits_of(a.data()[i])));
-    mag[static_cast<std::size_t>(i)] = std::isnan(m) ? HUGE_VALF : m;
-  }
-  std::vector<std::int64_t> order(static_cast<std::size_t>(total));
-  std::iota(order.begin(), order.end(), std::int64_t{0});
-  std::nth_element(order.begin(), order.begin() + (cut - 1), order.end(), [&](std::int64_t i, std::int64_t j) {
-    const float mi = mag[static_cast<std::size_t>(i)], mj = mag[static_cast<std::size_t>(j)];
-    return mi != mj ? mi < mj : i > j;
-  });
-  for (std::int64_t i = 0; i < cut; ++i) out.data()[order[static_cast<std::size_t>(i)]] = half_from_bits(kHalfPosZero);
+  HalfMatrix out(rows, cols);
+  gen_into(static_cast<std::int64_t>(rows) * cols, beta, seed, reinterpret_cast<std::uint16_t*>(out.data()));
   return out;
 }
 
@@ -120,3 +104,10 @@ HalfMatrix normalize_zeros(HalfMatrix a) {  // proj/src/matrix.cpp:111-116
 }
 
 }  // namespace tcsl
+
+// C entry point of the host library for bindings (include/tcsl_host.h).
+extern "C" int tcsl_host_gen_random_sparse(int rows, int cols, double beta, std::uint64_t seed, std::uint16_t* out) {
+  if (rows <= 0 || cols <= 0 || !out || !(beta >= 0.0 && beta <= 1.0)) return 10;  // Errc::invalid_argument + 1
+  tcsl::gen_into(static_cast<std::int64_t>(rows) * cols, beta, seed, out);
+  return 0;
+}

@@ -50,24 +50,36 @@ def max_rows(plan: list[Shard]) -> int:
     return max(s.rows for s in plan)
 
 
-def allgather_rows(y_local, plan: list[Shard], group=None):
+def allgather_rows(y_local, plan: list[Shard], group=None, comm=None, out=None):
     """All-gather row shards of Y (torch tensors, [rows_r, n]) into the full Y.
 
-    Shards are padded to the largest shard so a single all_gather_into_tensor
-    (one NCCL call) moves everything; padding rows are dropped afterwards."""
+    comm: a paper_2309_10285_b200.RowComm — the C-ABI's tcsl_cuda_allgather_rows
+    (one ncclAllGather, stream-ordered). Without it, torch.distributed on `group`
+    (NCCL or gloo). When every shard has the same row count (m / G a multiple of
+    128, as in BASELINE configs[4]) the gathered buffer IS Y (rank-major rows) and
+    no copy is made; ragged plans pad to the largest shard and drop the padding."""
     import torch
     import torch.distributed as dist
 
     world = len(plan)
     n = y_local.shape[1]
     rmax = max_rows(plan)
-    pad = torch.zeros((rmax, n), dtype=y_local.dtype, device=y_local.device)
-    pad[: y_local.shape[0]].copy_(y_local)
-    full = torch.empty((world * rmax, n), dtype=y_local.dtype, device=y_local.device)
-    if dist.get_backend(group) == "nccl":
+    uniform = all(s.rows == rmax for s in plan)
+    if uniform:
+        pad = y_local
+        full = out if out is not None else torch.empty((world * rmax, n), dtype=y_local.dtype, device=y_local.device)
+    else:
+        pad = torch.zeros((rmax, n), dtype=y_local.dtype, device=y_local.device)
+        pad[: y_local.shape[0]].copy_(y_local)
+        full = torch.empty((world * rmax, n), dtype=y_local.dtype, device=y_local.device)
+    if comm is not None:
+        comm.allgather_rows(pad, full)
+    elif dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(full, pad, group=group)
     else:
         dist.all_gather(list(full.chunk(world)), pad, group=group)
+    if uniform:
+        return full
     parts = [full[s.rank * rmax: s.rank * rmax + s.rows] for s in plan]
     return torch.cat(parts, dim=0)
 
@@ -76,20 +88,21 @@ class RowShardedSpmm:
     """One rank's part of a row-sharded SpMM on the GPU: holds the rank's
     Tiled-CSL shard (device), runs the tcgen05 SpMM on it and all-gathers Y."""
 
-    def __init__(self, t_full, world: int, rank: int, group=None):
+    def __init__(self, t_full, world: int, rank: int, group=None, comm=None):
         from . import shard_rows
         self.plan = shard_plan(t_full.m, t_full.cfg.m_tb, world)
         self.shard = self.plan[rank]
         self.group = group
+        self.comm = comm  # RowComm: the C-ABI NCCL all-gather (else torch.distributed)
         self.local = shard_rows(t_full, self.shard.tr0, self.shard.tr1) if self.shard.rows else None
         self.m = t_full.m
 
-    def __call__(self, x, split_k: int = 0):
+    def __call__(self, x, split_k: int = 0, out_dtype=None):
         import torch
 
         from . import spmm
         if self.local is not None:
-            y = spmm(self.local, x, split_k=split_k)
+            y = spmm(self.local, x, split_k=split_k, out_dtype=out_dtype)
         else:
-            y = torch.empty((0, x.shape[1]), dtype=torch.float32, device=x.device)
-        return allgather_rows(y, self.plan, self.group)
+            y = torch.empty((0, x.shape[1]), dtype=out_dtype or torch.float32, device=x.device)
+        return allgather_rows(y, self.plan, self.group, comm=self.comm)

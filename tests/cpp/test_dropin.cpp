@@ -172,6 +172,48 @@ int main() {
     }
   }
 
+  {  // prune_magnitude on the GPU (proj/tests/test_matrix.cpp:54-104)
+    HalfMatrix a(2, 2);
+    a(0, 0) = Eigen::half(1.0f);
+    a(0, 1) = Eigen::half(-4.0f);
+    a(1, 0) = Eigen::half(2.0f);
+    a(1, 1) = Eigen::half(3.0f);
+    const HalfMatrix p = prune_magnitude(a, 0.5);
+    CHECK(bits_of(p(0, 0)) == 0x0000 && bits_of(p(0, 1)) == 0xC400 && bits_of(p(1, 0)) == 0x0000 &&
+          bits_of(p(1, 1)) == 0x4200);
+    HalfMatrix t(1, 4);
+    for (int j = 0; j < 4; ++j) t(0, j) = Eigen::half(2.0f);
+    const HalfMatrix q = prune_magnitude(t, 0.5);
+    CHECK(bits_of(q(0, 0)) == 0x4000 && bits_of(q(0, 1)) == 0x4000 && bits_of(q(0, 2)) == 0 && bits_of(q(0, 3)) == 0);
+    CHECK(thrown([&] { prune_magnitude(t, 1.5); }) == Errc::invalid_argument);
+    HalfMatrix n(1, 4);
+    n(0, 0) = half_from_bits(kHalfQuietNan);
+    n(0, 1) = Eigen::half(1.0f);
+    n(0, 2) = Eigen::half(2.0f);
+    n(0, 3) = Eigen::half(3.0f);
+    const HalfMatrix pn = prune_magnitude(n, 0.5);
+    CHECK(f16_is_nan(bits_of(pn(0, 0))) && bits_of(pn(0, 1)) == 0 && bits_of(pn(0, 2)) == 0 && bits_of(pn(0, 3)) == 0x4200);
+  }
+
+  {  // a location repeated inside a tile: last writer wins, like extract_tile (engine.cpp:17-22)
+    const HalfMatrix a = gen_random_sparse(256, 128, 0.7, 31);
+    TcslMatrix t = encode(a);
+    for (std::uint32_t e = t.tile_offsets[0] + 1; e < t.tile_offsets[1]; e += 3)
+      t.entries[e] = TcslEntry::make(t.entries[e].value_bits(), t.entries[e - 1].location());
+    const HalfMatrix b = gen_random_sparse(128, 16, 0.0, 32);
+    const FloatMatrix want = dense_gemm_ref(decode(t), b);
+    CHECK(same(spmm(t, b), want));  // routed to the bit-exact path
+    HalfMatrix dense(256, 128);
+    dense.setZero();
+    for (std::uint32_t tile = 0; tile < t.num_tiles(); ++tile) {
+      const std::vector<HalfBits> d = extract_tile(t, tile);
+      const int r0 = static_cast<int>(tile) / t.tiles_k() * 128, c0 = static_cast<int>(tile) % t.tiles_k() * 64;
+      for (int x = 0; x < 128; ++x)
+        for (int y = 0; y < 64; ++y) dense(r0 + x, c0 + y) = half_from_bits(d[static_cast<std::size_t>(x) * 64 + y]);
+    }
+    CHECK(same(decode(t), dense));
+  }
+
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

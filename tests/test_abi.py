@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     L = tc.lib()
     for name in declared_functions():
         assert hasattr(L, name), name
-    assert L.tcsl_cuda_abi_version() == 1
+    assert L.tcsl_cuda_abi_version() == 2
     assert L.tcsl_cuda_status_string(8) == b"location out of range"
 
 

@@ -25,8 +25,22 @@ def test_dropin_builds_and_links():
     assert os.access(exe, os.X_OK)
     syms = subprocess.run(["nm", "-DC", os.path.join(LIB, "libtcsl.so")], capture_output=True, text=True).stdout
     for name in ("tcsl::encode(", "tcsl::decode(", "tcsl::spmm(", "tcsl::dense_gemm_ref(", "tcsl::serialize_tcsl(",
-                 "tcsl::deserialize_tcsl(", "tcsl::extract_tile(", "tcsl::reg_pressure(", "tcsl::gen_random_sparse("):
+                 "tcsl::deserialize_tcsl(", "tcsl::extract_tile(", "tcsl::reg_pressure(", "tcsl::gen_random_sparse(",
+                 "tcsl::prune_magnitude("):
         assert name in syms, name
+
+
+def test_dropin_half_conversions_cpu():
+    """a8: the drop-in's host binary16 conversions against the reference's
+    test_half.cpp cases (exhaustive decode, strided sweep, every midpoint)."""
+    build_exe()
+    exe = os.path.join(LIB, "test_half_dropin")
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT}/include", os.path.join(ROOT, "tests", "cpp",
+                    "test_half_dropin.cpp"), "-o", exe, f"-L{LIB}", "-ltcsl", "-ltcsl_cuda", f"-Wl,-rpath,{LIB}"],
+                   check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
 
 
 @pytest.mark.gpu

@@ -152,9 +152,13 @@ def test_errors(port):
     with pytest.raises(tc.TcslError, match="location_out_of_range"):
         tc.spmm(bad, _dev(port.gen_random_sparse(128, 8, 0.0, 2)))
     bad2 = tc.TcslMatrix(t.m, t.k, t.cfg, True, t.offsets.clone(), t.entries.clone())
-    bad2.offsets[1] += 16  # tile count no longer a whole number of groups
+    bad2.offsets[1] = t.n_entries + 32  # tile 0's span runs past the entries (engine.cpp:11-14)
     with pytest.raises(tc.TcslError, match="inconsistent_offsets"):
         tc.spmm(bad2, _dev(port.gen_random_sparse(128, 8, 0.0, 2)))
+    with pytest.raises(tc.TcslError, match="invalid_argument"):
+        tc.spmm(t, torch.zeros((128, 8), dtype=torch.bfloat16, device="cuda"))  # binary16 only
+    with pytest.raises(tc.TcslError, match="invalid_argument"):
+        tc.spmm(t, _dev(port.gen_random_sparse(128, 8, 0.0, 2)), out=torch.empty((256, 4), device="cuda"))
 
 
 def test_sharded_rows_match_full(port):
