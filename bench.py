@@ -1,27 +1,35 @@
 """Benchmark of the B200 Tiled-CSL SpMM (Flash-LLM LSCD) against BASELINE.json.
 
-Workload (BASELINE.json configs[1], the config its metric is quoted on): the
-four OPT-66B decoder MatMuls — QKV 27648x9216, out 9216x9216, FFN1 36864x9216,
-FFN2 9216x36864 — at N = 8/16/32/64 and 70/80/90 % sparsity: 48 SpMMs per step.
-Weights are synthetic random-sparse binary16 (reference value law) generated
-and encoded on the GPU; X is synthetic binary16. Metric: TFLOPS = sum 2MKN /
-sum t (dense-equivalent), plus GB/s of the algorithmic bytes
-4E + 4(T+1) + 2KN + 4MN.
+Workload (BASELINE.json metric "SpMM TFLOPS (2MKN/t) + HBM GB/s, OPT-66B/175B
+shapes, N=8-64, 70-90% sparse"): configs[1] — the four OPT-66B decoder MatMuls
+(QKV 27648x9216, out 9216x9216, FFN1 36864x9216, FFN2 9216x36864) — and
+configs[3] — the three OPT-175B MatMuls (QKV 36864x12288, FFN1 49152x12288, FFN2
+12288x49152) — at N = 8/16/32/64 and 70/80/90 % sparsity: 84 SpMMs per step.
+
+Inputs are the reference's own generator bits: W = gen_random_sparse(M, K, beta,
+seed 1), X = gen_random_sparse(K, N, 0, seed 2) (proj/src/matrix.cpp:35-67), made
+by the drop-in host library (libtcsl.so, bit-identical to the reference; the GPU
+parity tests check these exact inputs against the CPU oracle), encoded on the GPU.
+Metric: TFLOPS = sum 2MKN / time (dense-equivalent), plus GB/s of
+the algorithmic bytes 4E + 4(T+1) + 2KN + 4MN.
 
   python bench.py [--gpus N --steps K --warmup W]          # our arm
   python bench.py --impl reference [...]                    # reference CPU arm
 Under torchrun (N > 1) every matrix is row-sharded across the ranks and Y is
-all-gathered with NCCL (BASELINE.json north_star (4)); rank 0 prints one JSON line.
+all-gathered through the C-ABI's NCCL entry point (BASELINE.json north_star (4));
+rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -29,24 +37,31 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SpMM TFLOPS (2MKN/t) + HBM GB/s, OPT-66B/175B shapes, N=8-64, 70-90% sparse"
-SHAPES = {"qkv": (27648, 9216), "out": (9216, 9216), "ffn1": (36864, 9216), "ffn2": (9216, 36864)}
-# SURVEY.md §8d C4 (side suite, --suite opt175b; the default line stays on configs[1])
-SHAPES_175B = {"qkv": (36864, 12288), "ffn1": (49152, 12288), "ffn2": (12288, 49152)}
-WORKLOAD_175B = "OPT-175B QKV/FFN1/FFN2 SpMMs x N{8,16,32,64} x sparsity{0.7,0.8,0.9} (36 per step)"
+SHAPES_66B = {"qkv": (27648, 9216), "out": (9216, 9216), "ffn1": (36864, 9216), "ffn2": (9216, 36864)}
+SHAPES_175B = {"qkv175": (36864, 12288), "ffn1_175": (49152, 12288), "ffn2_175": (12288, 49152)}
+SUITES = {
+    "all": ({**SHAPES_66B, **SHAPES_175B},
+            "OPT-66B (configs[1]) + OPT-175B (configs[3]) SpMMs: 7 shapes x N{8,16,32,64} x sparsity{0.7,0.8,0.9} "
+            "(84 per step)"),
+    "opt66b": (SHAPES_66B, "OPT-66B QKV/out/FFN1/FFN2 SpMMs x N{8,16,32,64} x sparsity{0.7,0.8,0.9} (48 per step)"),
+    "opt175b": (SHAPES_175B, "OPT-175B QKV/FFN1/FFN2 SpMMs x N{8,16,32,64} x sparsity{0.7,0.8,0.9} (36 per step)"),
+}
+SHAPES, WORKLOAD = SUITES["all"]
 NS = [8, 16, 32, 64]
 BETAS = [0.7, 0.8, 0.9]
-WORKLOAD = "OPT-66B QKV/out/FFN1/FFN2 SpMMs x N{8,16,32,64} x sparsity{0.7,0.8,0.9} (48 per step)"
+SEED_W, SEED_X = 1, 2
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-FALLBACK_HBM, FALLBACK_TC = 6650.0, 1590.0
+FALLBACK_HBM, FALLBACK_TC = 6650.0, 1590.0  # B200_PROFILING.md fallbacks (GB/s, dense bf16 TF/s)
+CPU_ROWS_PER_THREAD = 128
 
 
 def peaks():
     try:
         with open(PEAKS_PATH) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return FALLBACK_HBM, FALLBACK_TC, "fallback"
+        return FALLBACK_HBM, FALLBACK_TC, "fallback (B200_PROFILING.md)"
 
 
 def parse_only(spec):
@@ -59,13 +74,87 @@ def parse_only(spec):
 
 
 def cell_list(args):
+    """N outermost: between two uses of one compressed weight every other weight of
+    the step streams through HBM, so no cell reads its weight from L2."""
     if args.only:
         return parse_only(args.only)
-    return [(name, beta, n) for beta in BETAS for name in SHAPES for n in NS]
+    return [(name, beta, n) for n in NS for beta in BETAS for name in SHAPES]
 
 
+def weight_list(cells):
+    seen = []
+    for name, beta, _ in cells:
+        if (name, beta) not in seen:
+            seen.append((name, beta))
+    return seen
+
+
+def alg_bytes(t, n):
+    return 4 * t.n_entries + 4 * (t.num_tiles + 1) + 2 * t.k * n + 4 * t.m * n
+
+
+def flops_of(m, k, n):
+    return 2.0 * m * k * n
+
+
+def bench_config(args, world):
+    """The `config` object of the JSON line; identical for both arms (the reference
+    arm's sampling is described in its cpu_baseline.sample)."""
+    return {"workload": WORKLOAD, "tile": "128x64 Tiled-CSL, bank-reordered", "n_cells": len(cell_list(args)),
+            "inputs": "gen_random_sparse(M,K,beta,seed 1), X = gen_random_sparse(K,N,0,seed 2)",
+            "l2": "cold: cells run N-outer, so each compressed weight is re-read only after every other weight "
+                  "of the step (GBs) has streamed; per-cell times read a 256 MB buffer (2x L2) before each replay",
+            "parallelism": "single GPU" if world == 1 else f"row-shard x{world} + NCCL all-gather of Y (C-ABI)"}
+
+
+# ------------------------------------------------------------------------------ host inputs
+_host_lib = None
+
+
+def host_lib():
+    """The C++ drop-in host library (its C entry point, include/tcsl_host.h)."""
+    global _host_lib
+    if _host_lib is None:
+        path = os.path.join(ROOT, "paper_2309_10285_b200", "_lib", "libtcsl.so")
+        L = C.CDLL(path)
+        L.tcsl_host_gen_random_sparse.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_void_p]
+        L.tcsl_host_gen_random_sparse.restype = C.c_int
+        _host_lib = L
+    return _host_lib
+
+
+def gen_random_sparse(rows, cols, beta, seed):
+    out = np.empty((rows, cols), np.uint16)
+    st = host_lib().tcsl_host_gen_random_sparse(rows, cols, beta, seed, out.ctypes.data)
+    if st:
+        raise RuntimeError(f"gen_random_sparse failed ({st})")
+    return out
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------------------ clocks
 class ClockSampler:
     """NVML SM-clock / throttle-reason sampler running during the timed region."""
+
+    NAMES = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+             0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
 
     def __init__(self, index=0, period=0.005):
         self.samples, self.reasons, self.period = [], set(), period
@@ -81,17 +170,13 @@ class ClockSampler:
             self.max_mhz = None
         self._stop = threading.Event()
 
-    NAMES = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
-             0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
-             0x1: "gpu_idle"}
-
     def _run(self):
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.NAMES.items():
-                    if r & bit and bit != 0x1:
+                    if r & bit:
                         self.reasons.add(name)
             except Exception:
                 pass
@@ -115,167 +200,207 @@ class ClockSampler:
 
 def ncu_traffic():
     """DRAM bytes per launch of the SpMM kernel from the newest committed ncu --set full
-    summary (profiles/*_ncu_*.json, written by tools/ncu_summary.py), or None."""
+    summary of the reference cell (profiles/*_ncu_*ffn1_b08_n16.json), or None."""
     import glob
     import re
 
-    def version(path):  # r01_ncu_v15_ffn1_b08_n16.json -> 15 (file mtimes do not survive copies)
-        m = re.search(r"_v(\d+)[a-z]?_", os.path.basename(path))
-        return int(m.group(1)) if m else -1
+    def version(path):  # r02_ncu_v3_ffn1_b08_n16.json -> (2, 3)
+        m = re.search(r"r(\d+)_ncu_v(\d+)[a-z]?_", os.path.basename(path))
+        return (int(m.group(1)), int(m.group(2))) if m else (-1, -1)
 
-    files = glob.glob(os.path.join(ROOT, "profiles", "*_ncu_*.json"))
-    ref = [f for f in files if "_ffn1_b08_n16" in f]  # the reference cell of the summaries
-    files = sorted(ref or files, key=version)
+    files = [f for f in glob.glob(os.path.join(ROOT, "profiles", "*_ncu_*.json")) if "_ffn1_b08_n16" in f]
     if not files:
         return None
     try:
-        with open(files[-1]) as f:
+        path = sorted(files, key=version)[-1]
+        with open(path) as f:
             d = json.load(f)
         return {"dram_bytes_per_launch": d["dram_bytes_per_launch"], "alg_bytes_per_launch": d["alg_bytes_per_launch"],
-                "cell": d.get("cell", ""), "source": os.path.relpath(files[-1], ROOT)}
+                "cell": d.get("cell", ""), "source": os.path.relpath(path, ROOT)}
     except Exception:
         return None
 
 
-def alg_bytes(t, n):
-    return 4 * t.n_entries + 4 * (t.num_tiles + 1) + 2 * t.k * n + 4 * t.m * n
+# ------------------------------------------------------------------------------ our arm
+def prepare_weights(tc, torch, dev, weights, rank, world, keep_rows):
+    """Generate every weight on the host (reference generator, a thread per weight),
+    upload, encode on the GPU (K1) and keep its row shard. Returns the shards, the K1
+    timings and the first `keep_rows` rows of each weight (for the CPU baseline)."""
+    from paper_2309_10285_b200.sharding import shard_plan
+
+    def gen(key):
+        m, k = SHAPES[key[0]]
+        return gen_random_sparse(m, k, key[1], SEED_W)
+
+    mats, enc, head = {}, {}, {}
+    workers = max(1, min(len(weights), cpu_threads() // max(1, world)))
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        futs = {key: ex.submit(gen, key) for key in weights}
+        for key in weights:
+            a = futs.pop(key).result()
+            m, k = SHAPES[key[0]]
+            plan = shard_plan(m, 128, world)
+            sh = plan[rank]
+            if keep_rows:
+                head[key] = a[:keep_rows].copy()
+            w = torch.from_numpy(a[sh.row0:sh.row0 + sh.rows].view(np.int16)).to(dev)
+            del a
+            tc.encode(w)  # warm (allocations, tensor-map setup)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            t = tc.encode(w)
+            e1.record()
+            torch.cuda.synchronize()
+            enc[key] = (e0.elapsed_time(e1) * 1e3, 2 * w.numel(), t.n_entries)
+            mats[key] = (t, sh, plan)
+            del w
+    return mats, enc, head
 
 
-# ---------------------------------------------------------------------------------------- our arm
 def run_ours(args, rank, world):
     import torch
-    import torch.distributed as dist
 
     import paper_2309_10285_b200 as tc
+    from paper_2309_10285_b200.sharding import allgather_rows
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     cells = cell_list(args)
+    weights = weight_list(cells)
     hbm_peak, tc_peak, peak_kind = peaks()
+    threads = max(1, min(cpu_threads(), 64))
+    keep_rows = threads * CPU_ROWS_PER_THREAD if (rank == 0 and world == 1 and not args.no_cpu_baseline) else 0
+    mats, enc, head = prepare_weights(tc, torch, dev, weights, rank, world, keep_rows)
 
-    # ---- setup: synthetic weights generated + encoded on the GPU (row shard per rank)
-    from paper_2309_10285_b200.sharding import shard_plan
-
-    mats, plans = {}, {}
-    for name, beta, n in cells:
-        if (name, beta) in mats:
-            continue
-        M, K = SHAPES[name]
-        plan = shard_plan(M, 128, world)
-        sh = plan[rank]
-        w = tc.gen_synthetic(max(sh.rows, 1), K, beta, seed=hash((name, beta, rank)) & 0xFFFFFFFF)
-        mats[(name, beta)] = (tc.encode(w), sh.row0, sh.rows)
-        plans[(name, beta)] = plan
-        del w
-    torch.cuda.synchronize()
-    xs, ys, gathered, wss = {}, {}, {}, {}
+    comm = tc.RowComm(rank, world) if world > 1 else None
+    xs, ys, gathered, wss, hx = {}, {}, {}, {}, {}
     for name, beta, n in cells:
         M, K = SHAPES[name]
         if (K, n) not in xs:
-            xs[(K, n)] = tc.gen_synthetic(K, n, 0.0, seed=K * 131 + n)
-        t, r0, rows = mats[(name, beta)]
+            hx[(K, n)] = gen_random_sparse(K, n, 0.0, SEED_X)
+            xs[(K, n)] = torch.from_numpy(hx[(K, n)].view(np.int16)).to(dev)
+        t, sh, plan = mats[(name, beta)]
         ys[(name, beta, n)] = torch.empty((t.m, n), dtype=torch.float32, device=dev)
         wss[(name, beta, n)] = tc.SpmmWorkspace()
         if world > 1:
-            rmax = max(s.rows for s in plans[(name, beta)])
-            gathered[(name, beta, n)] = (torch.empty((world * rmax, n), dtype=torch.float32, device=dev),
-                                         torch.zeros((rmax, n), dtype=torch.float32, device=dev))
+            gathered[(name, beta, n)] = torch.empty((world * max(s.rows for s in plan), n), dtype=torch.float32,
+                                                    device=dev)
 
     def one_cell(name, beta, n):
-        # row-sharded SpMM (paper_2309_10285_b200.sharding): local rows, then one
-        # NCCL all-gather of the padded row shards (buffers preallocated so the
-        # whole step can be captured in a CUDA graph)
-        t, r0, rows = mats[(name, beta)]
+        t, sh, plan = mats[(name, beta)]
         y = ys[(name, beta, n)]
         tc.spmm(t, xs[(SHAPES[name][1], n)], split_k=args.split, out=y, ws=wss[(name, beta, n)], check=False)
         if world > 1:
-            full, pad = gathered[(name, beta, n)]
-            pad[:rows].copy_(y[:rows])
-            dist.all_gather_into_tensor(full, pad)
+            allgather_rows(y, plan, comm=comm, out=gathered[(name, beta, n)])
 
     def step():
         for c in cells:
             one_cell(*c)
 
-    # correctness gate before timing: device error words clean, results finite
+    # correctness gate before timing: device error words clean
     for c in cells:
-        t, r0, rows = mats[(c[0], c[1])]
+        t = mats[(c[0], c[1])][0]
         tc.spmm(t, xs[(SHAPES[c[0]][1], c[2])], split_k=args.split, out=ys[c], ws=wss[c], check=True)
     torch.cuda.synchronize()
 
-    use_graph = not args.no_graph
     graph = None
-    if use_graph:
-        try:
+    if not args.no_graph:
+        step()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
             step()
-            torch.cuda.synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                step()
-            torch.cuda.synchronize()
-        except Exception as e:  # pragma: no cover - eager fallback
-            print(f"[bench] graph capture failed ({e}); running eager", file=sys.stderr)
-            graph = None
+        torch.cuda.synchronize()
     run = graph.replay if graph is not None else step
 
-    for _ in range(args.warmup):
+    for _ in range(max(3, args.warmup)):
         run()
     torch.cuda.synchronize()
     if world > 1:
-        dist.barrier()
+        torch.distributed.barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clocks:
+        torch.cuda.synchronize()
         start.record()
         for _ in range(args.steps):
             run()
         end.record()
         torch.cuda.synchronize()
     if world > 1:
-        dist.barrier()
+        torch.distributed.barrier()
     ms = start.elapsed_time(end) / args.steps
     if world > 1:
         tms = torch.tensor([ms], device=dev)
-        dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+        torch.distributed.all_reduce(tms, op=torch.distributed.ReduceOp.MAX)
         ms = float(tms.item())
 
-    flops = sum(2.0 * SHAPES[nm][0] * SHAPES[nm][1] * n for nm, b, n in cells)
+    flops = sum(flops_of(*SHAPES[nm], n) for nm, b, n in cells)
     launches_per_step = 0
     for nm, b, n in cells:
         t = mats[(nm, b)][0]
         launches_per_step += 1 + ((args.split or tc.auto_split(t.m, t.k, n)) > 1)
     total_alg = sum(alg_bytes(mats[(nm, b)][0], n) for nm, b, n in cells)
 
-    # ---- per-SpMM device times (L2 flushed before each), roofline of the SpMM kernel.
-    # Each cell is replayed from its own CUDA graph so host launch overhead never
-    # sits between the start event and the kernel (the flush keeps the GPU busy).
-    cell_graphs = {}
-    if world == 1 and graph is not None:
-        for c in cells:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                one_cell(*c)
-            cell_graphs[c] = g
-        torch.cuda.synchronize()
-    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    cell_rows, sum_t, sum_bytes = [], 0.0, 0
-    reps = max(3, args.kernel_reps)
-    for nm, b, n in cells:
-        t = mats[(nm, b)][0]
-        times = []
+    result = {
+        "metric": METRIC,
+        "value": round(flops / (ms * 1e-3) / 1e12, 3),
+        "unit": "TFLOPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f16 in / f32 accumulate / f32 out",
+        "data": "synthetic: the reference's gen_random_sparse bits (seeds 1 / 2) via the drop-in host library",
+        "config": bench_config(args, world),
+        "hbm_gbs": round(total_alg / (ms * 1e-3) / 1e9, 1),
+        "gpu_launches": launches_per_step * args.steps + (len(cells) * args.steps if world > 1 else 0),
+        "clocks": clocks.summary(),
+    }
+    if world > 1 or args.quick:
+        return result
+
+    # ---- per-SpMM device times, cold: each replay is preceded by a 256 MB read (2x L2, clean
+    # lines, so no write-back lands in the cell). t_cell = (T[read+cell] - T[read]) / R over
+    # R replays inside one event pair (well above the ~2 us timer quantum).
+    flush = torch.zeros(32 * 1024 * 1024, dtype=torch.int64, device=dev)  # 256 MB, read-only below
+    sink = torch.empty((), dtype=torch.int64, device=dev)
+    R = max(4, args.kernel_reps)
+
+    def read_flush():
+        torch.sum(flush, dim=0, out=sink)
+
+    def graph_of(fn, reps):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(reps):
+                fn()
+        return g
+
+    def timed(g, reps=3):
+        out = []
         for _ in range(reps):
-            flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            if (nm, b, n) in cell_graphs:
-                cell_graphs[(nm, b, n)].replay()
-            else:
-                tc.spmm(t, xs[(t.k, n)], split_k=args.split, out=ys[(nm, b, n)], ws=wss[(nm, b, n)], check=False)
+            g.replay()
             e1.record()
             torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1) * 1e3)
-        us = statistics.median(times)
+            out.append(e0.elapsed_time(e1) * 1e3)
+        return statistics.median(out)
+
+    g_flush = graph_of(read_flush, R)
+    t_flush = timed(g_flush, 5) / R
+    cell_rows, sum_t, sum_bytes = [], 0.0, 0
+    for nm, b, n in cells:
+        t = mats[(nm, b)][0]
+        g = graph_of(lambda: (read_flush(), one_cell(nm, b, n)), R)
+        us = max(timed(g) / R - t_flush, 1e-3)
+        del g
         nbytes = alg_bytes(t, n)
-        fl = 2.0 * t.m * t.k * n
+        fl = flops_of(t.m, t.k, n)
         t_hbm = nbytes / (hbm_peak * 1e3)  # us
         t_tc = fl / (tc_peak * 1e6)
         cell_rows.append({"shape": nm, "M": t.m, "K": t.k, "N": n, "sparsity": b, "E": t.n_entries,
@@ -284,257 +409,221 @@ def run_ours(args, rank, world):
                           "hbm_frac": round(t_hbm / us, 3), "roofline_frac": round(max(t_hbm, t_tc) / us, 3)})
         sum_t += us
         sum_bytes += nbytes
+    torch.cuda.synchronize()
 
-    # ---- cuBLAS dense fp16 on the same shapes (context only)
-    if not args.no_cublas and world == 1:
-        for nm in sorted({c[0] for c in cells}):
+    # ---- cuBLAS dense fp16 on the same shapes (context only; the same cold protocol)
+    if not args.no_cublas:
+        for nm in SHAPES:
+            if not any(r["shape"] == nm for r in cell_rows):
+                continue
             M, K = SHAPES[nm]
             wd = torch.randn((M, K), dtype=torch.float16, device=dev)
             for row in cell_rows:
                 if row["shape"] != nm:
                     continue
                 x = xs[(K, row["N"])].view(torch.float16)
-                times = []
-                for _ in range(reps):
-                    flush.zero_()
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record()
-                    torch.matmul(wd, x)
-                    e1.record()
-                    torch.cuda.synchronize()
-                    times.append(e0.elapsed_time(e1) * 1e3)
-                row["cublas_dense_fp16_us"] = round(statistics.median(times), 2)
+                yd = torch.empty((M, row["N"]), dtype=torch.float16, device=dev)
+                torch.matmul(wd, x, out=yd)  # cuBLAS handle / workspace before capture
+                torch.cuda.synchronize()
+                g = graph_of(lambda: (read_flush(), torch.matmul(wd, x, out=yd)), R)
+                row["cublas_dense_fp16_us"] = round(max(timed(g) / R - t_flush, 1e-3), 2)
                 row["speedup_vs_cublas"] = round(row["cublas_dense_fp16_us"] / row["us"], 2)
+                del g
             del wd
     del flush
 
-    # ---- end-to-end through the public API with HOST buffers (pinned), our arm only at N=1
-    e2e = None
-    if world == 1 and not args.no_e2e:
-        e2e = run_e2e(args, tc, mats, xs, cells, dev)
-
     traffic = ncu_traffic()
-    result = {
-        "metric": METRIC,
-        "value": round(flops / (ms * 1e-3) / 1e12, 3),
-        "unit": "TFLOPS",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": round(ms, 4),
-        "higher_is_better": True,
-        "scaling": "strong",
-        "vs_baseline": None,
-        "dtype": "f16",
-        "data": "synthetic (GPU-generated random-sparse binary16 with the reference value law; seeded)",
-        "config": {"workload": WORKLOAD, "tile": "128x64 Tiled-CSL, bank-reordered", "n_cells": len(cells),
-                   "l2": "inputs larger than L2: every step streams the distinct compressed weights of all "
-                         "cells (%.2f GB); per-kernel timings flush L2 (512 MB write) first" %
-                         (sum(4 * mats[k][0].n_entries for k in mats) / 1e9),
-                   "parallelism": "single GPU" if world == 1 else f"row-shard x{world} + NCCL all-gather of Y",
-                   "graph": graph is not None},
-        "hbm_gbs": round(total_alg / (ms * 1e-3) / 1e9, 1),
-        "roofline": {"bound": "hbm", "achieved": round(sum_bytes / sum_t / 1e3, 1), "peak": hbm_peak,
-                     "unit": "GB/s", "frac": round(sum_bytes / sum_t / 1e3 / hbm_peak, 3),
-                     "traffic": (traffic or {}).get("dram_bytes_per_launch"),
-                     "traffic_detail": traffic, "peak_kind": peak_kind,
-                     "kernel": "tcsl spmm_sm100_kernel (+ split-K reduce when split>1)",
-                     "bytes_per_launch": "4E + 4(T+1) + 2KN + 4MN",
-                     # time-weighted fraction of max(t_HBM, t_TC) (tensor-bound cells included)
-                     "max_hbm_tc_frac": round(sum(r["roofline_frac"] * r["us"] for r in cell_rows) / sum_t, 3)},
-        "gpu_launches": launches_per_step * args.steps,
-        "clocks": clocks.summary(),
-        "cells": cell_rows,
+    achieved = sum_bytes / sum_t / 1e3
+    by_beta = {}
+    for b in BETAS:
+        rows = [r for r in cell_rows if r["sparsity"] == b]
+        if rows:
+            by_beta[str(b)] = round(sum(r["gbs"] * r["us"] for r in rows) / sum(r["us"] for r in rows) / hbm_peak, 3)
+    result["roofline"] = {
+        "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+        "frac": round(achieved / hbm_peak, 3), "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+        "traffic_detail": traffic, "peak_kind": peak_kind,
+        "kernel": "tcsl spmm_sm100_kernel (+ split-K reduce when split>1)",
+        "bytes_per_launch": "4E + 4(T+1) + 2KN + 4MN (SURVEY.md §8d), per cell; achieved = sum bytes / sum cold us",
+        "frac_by_sparsity": by_beta,
+        "max_hbm_tc_frac": round(sum(r["roofline_frac"] * r["us"] for r in cell_rows) / sum_t, 3),
+        "sum_cold_cell_ms": round(sum_t / 1e3, 4),
     }
-    if e2e is not None:
-        result["e2e"] = e2e
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(args, quick=True)
+    result["cells"] = cell_rows
+    result["encoder"] = {
+        "kernel": "K1 tcsl_cuda_encode_count + scan + encode_emit (bit-exact Tiled-CSL)",
+        "weights": len(enc), "ms_total": round(sum(v[0] for v in enc.values()) / 1e3, 3),
+        "dense_gbs": round(sum(v[1] for v in enc.values()) / (sum(v[0] for v in enc.values()) * 1e3), 1),
+        "per_weight_us": {f"{k[0]}@{k[1]}": round(v[0], 1) for k, v in enc.items()},
+    }
+    if not args.no_e2e:
+        result["e2e"] = run_e2e(args, tc, torch, mats, hx, cells, dev)
+    if not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(head, cells, threads, steps=1)
     return result
 
 
-def run_e2e(args, tc, mats, xs, cells, dev):
-    """Drop-in path: host TcslMatrix + host X in, host Y out, copies inside the timed region."""
-    import torch
-    stream = torch.cuda.current_stream()
-    host = {}
-    for key, (t, r0, rows) in mats.items():
-        off = t.offsets.cpu().pin_memory()
-        ent = t.entries.cpu().pin_memory()
-        host[key] = (off, ent)
-    hx = {k: v.cpu().pin_memory() for k, v in xs.items()}
-    maxE = max(t.n_entries for t, _, _ in mats.values())
-    maxT = max(t.num_tiles for t, _, _ in mats.values())
-    d_ent = torch.empty(maxE, dtype=torch.int32, device=dev)
-    d_off = torch.empty(maxT + 1, dtype=torch.int32, device=dev)
-    hy = {c: torch.empty((mats[(c[0], c[1])][2], c[2]), dtype=torch.float32).pin_memory() for c in cells}
+def run_e2e(args, tc, torch, mats, hx, cells, dev):
+    """Through the public API with HOST buffers: every step uploads each cell's X from
+    pinned host memory, runs spmm on the resident weights and reads Y back into pinned
+    host memory (the serving call: weights are model state loaded once, e.g. with
+    paper_2309_10285_b200.load_tcsl). The drop-in variant that also re-uploads the
+    compressed weights on every call (tcsl::spmm's host TcslMatrix) is reported beside it."""
+    hxp = {k: torch.from_numpy(v.view(np.int16)).pin_memory() for k, v in hx.items()}
+    xdev = {k: torch.empty(v.shape, dtype=torch.int16, device=dev) for k, v in hxp.items()}
+    hy = {c: torch.empty((mats[(c[0], c[1])][0].m, c[2]), dtype=torch.float32).pin_memory() for c in cells}
     ws = tc.SpmmWorkspace()
-    xdev = {k: torch.empty_like(v, device=dev) for k, v in xs.items()}
-    h2d = d2h = 0
+    flops = sum(flops_of(*SHAPES[nm], n) for nm, b, n in cells)
+    h2d = sum(2 * hxp[(SHAPES[nm][1], n)].numel() for nm, b, n in cells)
+    d2h = sum(4 * hy[c].numel() for c in cells)
 
-    def step():
-        nonlocal h2d, d2h
-        h2d = d2h = 0
-        for nm, b, n in cells:
-            t, r0, rows = mats[(nm, b)]
-            off, ent = host[(nm, b)]
-            d_off[:off.numel()].copy_(off, non_blocking=True)
-            d_ent[:ent.numel()].copy_(ent, non_blocking=True)
-            xd = xdev[(t.k, n)]
-            xd.copy_(hx[(t.k, n)], non_blocking=True)
-            tt = tc.TcslMatrix(t.m, t.k, t.cfg, t.reordered, d_off[:off.numel()], d_ent[:ent.numel()])
-            y = tc.spmm(tt, xd, ws=ws, check=False)
-            hy[(nm, b, n)].copy_(y, non_blocking=True)
-            h2d += 4 * (off.numel() + ent.numel()) + 2 * xd.numel()
-            d2h += 4 * y.numel()
-
-    for _ in range(max(1, min(args.warmup, 2))):
-        step()
-    torch.cuda.synchronize()
-    steps = max(1, min(args.steps, 3))
-    t0 = time.perf_counter()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        step()
-    e1.record()
-    torch.cuda.synchronize()
-    wall = (time.perf_counter() - t0) / steps
-    ms = max(e0.elapsed_time(e1) / steps, wall * 1e3)
-    flops = sum(2.0 * SHAPES[nm][0] * SHAPES[nm][1] * n for nm, b, n in cells)
-    out = {"value": round(flops / (ms * 1e-3) / 1e12, 4), "unit": "TFLOPS", "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3), "steps": steps,
-           "api": "tcsl_cuda_spmm via paper_2309_10285_b200.spmm; compressed W + X uploaded from pinned host "
-                  "memory and Y read back every call (drop-in tcsl::spmm semantics)"}
-    # serving variant: weights resident on the device, X up / Y down per call
     def step_resident():
         for nm, b, n in cells:
             t = mats[(nm, b)][0]
             xd = xdev[(t.k, n)]
-            xd.copy_(hx[(t.k, n)], non_blocking=True)
+            xd.copy_(hxp[(t.k, n)], non_blocking=True)
             y = tc.spmm(t, xd, ws=ws, check=False)
             hy[(nm, b, n)].copy_(y, non_blocking=True)
-    step_resident()
-    torch.cuda.synchronize()
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(2):
+        step_resident()
+    steps = max(3, min(args.steps, 10))
     t0 = time.perf_counter()
     for _ in range(steps):
         step_resident()
-    torch.cuda.synchronize()
-    ms_r = (time.perf_counter() - t0) / steps * 1e3
-    out["resident_weights"] = {"value": round(flops / (ms_r * 1e-3) / 1e12, 3), "unit": "TFLOPS",
-                               "ms_per_step": round(ms_r, 3)}
+    ms = (time.perf_counter() - t0) / steps * 1e3
+    out = {"value": round(flops / (ms * 1e-3) / 1e12, 3), "unit": "TFLOPS", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3), "steps": steps, "clock": "host wall clock",
+           "api": "paper_2309_10285_b200.spmm (tcsl_cuda_spmm_ex): X pinned host -> device, Y device -> pinned "
+                  "host every call; weights resident"}
+
+    # drop-in tcsl::spmm semantics: the compressed weights cross PCIe on every call too
+    host = {key: (v[0].offsets.cpu().pin_memory(), v[0].entries.cpu().pin_memory()) for key, v in mats.items()}
+    maxE = max(v[0].n_entries for v in mats.values())
+    maxT = max(v[0].num_tiles for v in mats.values())
+    d_ent = torch.empty(maxE, dtype=torch.int32, device=dev)
+    d_off = torch.empty(maxT + 1, dtype=torch.int32, device=dev)
+    h2d_full = h2d + sum(4 * (host[(nm, b)][0].numel() + host[(nm, b)][1].numel()) for nm, b, n in cells)
+
+    def step_upload():
+        for nm, b, n in cells:
+            t = mats[(nm, b)][0]
+            off, ent = host[(nm, b)]
+            d_off[:off.numel()].copy_(off, non_blocking=True)
+            d_ent[:ent.numel()].copy_(ent, non_blocking=True)
+            xd = xdev[(t.k, n)]
+            xd.copy_(hxp[(t.k, n)], non_blocking=True)
+            # a fresh host-provided matrix: spmm validates it on the device (one pass over E)
+            tt = tc.TcslMatrix(t.m, t.k, t.cfg, t.reordered, d_off[:off.numel()], d_ent[:ent.numel()])
+            y = tc.spmm(tt, xd, ws=ws, check=False)
+            hy[(nm, b, n)].copy_(y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    step_upload()
+    t0 = time.perf_counter()
+    step_upload()
+    ms_u = (time.perf_counter() - t0) * 1e3
+    out["weights_uploaded_per_call"] = {"value": round(flops / (ms_u * 1e-3) / 1e12, 4), "unit": "TFLOPS",
+                                        "h2d_bytes_per_step": h2d_full, "d2h_bytes_per_step": d2h,
+                                        "ms_per_step": round(ms_u, 3), "steps": 1}
     return out
 
 
-# ---------------------------------------------------------------------------------------- CPU side
-def cpu_cores():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
+# ------------------------------------------------------------------------------ CPU side
+def cpu_sample_desc(nrows, threads, ncells):
+    return (f"{ncells} cells (every cell of the step), the first {nrows} rows of each weight "
+            f"(one 128-row block per thread), unmodified reference tcsl::spmm per row block; host: {cpu_model()}, "
+            f"{cpu_threads()} hardware threads, {threads} used")
 
 
-def cpu_model():
-    try:
-        with open("/proc/cpuinfo") as f:
-            for line in f:
-                if line.startswith("model name"):
-                    return line.split(":", 1)[1].strip()
-    except Exception:
-        pass
-    return "unknown"
-
-
-def ref_sample_cells(quick):
-    if quick:
-        return [(nm, 0.8, 16) for nm in SHAPES]
-    return [(nm, b, n) for b in BETAS for nm in SHAPES for n in NS]
-
-
-def cpu_baseline(args, quick=False, rows_per_thread=128):
-    """The reference tcsl::spmm (oracle/_ref, unmodified sources) timed on this host.
-
-    Sample: for each cell, a row slice of `threads` row blocks (128 rows each), one
-    reference tcsl::spmm per row block in its own thread (row blocks are independent)."""
+def cpu_baseline(head, cells, threads, steps=1):
+    """The reference's CPU tcsl::spmm (oracle/_ref: the unmodified reference sources;
+    else the C port) on a bounded sample of this workload: the first threads*128 rows
+    of every weight, every cell, one 128-row block per thread."""
     import oracle
     kind = "reference" if oracle.ref_available() else "port"
     impl = oracle.ref() if kind == "reference" else oracle.port()
-    threads = max(1, min(cpu_cores(), 64))
-    rows = threads * rows_per_thread
-    total_fl, total_s = 0.0, 0.0
-    cells = ref_sample_cells(quick)
-    for nm, b, n in cells:
-        M, K = SHAPES[nm]
-        seed = (hash((nm, b)) & 0xFFFF) + 1
-        a = impl.gen_random_sparse(rows, K, b, seed)
-        x = impl.gen_random_sparse(K, n, 0.0, seed + 1)
+    plans, xs = {}, {}
+    for key, a in head.items():
         t = impl.encode(a)
-        if kind == "reference":
-            plan = impl.spmm_plan(t, threads)
+        plans[key] = (impl.spmm_plan(t, threads), a.shape[0]) if kind == "reference" else (t, a.shape[0])
+    for name, beta, n in cells:
+        K = SHAPES[name][1]
+        if (K, n) not in xs:
+            xs[(K, n)] = gen_random_sparse(K, n, 0.0, SEED_X)
+    total_fl, total_s = 0.0, 0.0
+    for _ in range(steps):
+        for name, beta, n in cells:
+            plan, rows = plans[(name, beta)]
+            x = xs[(SHAPES[name][1], n)]
             y = np.empty((rows, n), np.float32)
             t0 = time.perf_counter()
-            impl.spmm_run(plan, x, rows, y)
-            dt = time.perf_counter() - t0
+            if kind == "reference":
+                impl.spmm_run(plan, x, rows, y)
+            else:
+                impl.spmm(plan, x, threads)
+            total_s += time.perf_counter() - t0
+            total_fl += flops_of(rows, SHAPES[name][1], n)
+    if kind == "reference":
+        for plan, _ in plans.values():
             impl.spmm_free(plan)
-        else:
-            t0 = time.perf_counter()
-            impl.spmm(t, x, threads)
-            dt = time.perf_counter() - t0
-        total_fl += 2.0 * rows * K * n
-        total_s += dt
+    nrows = next(iter(head.values())).shape[0]
     return {"value": round(total_fl / total_s / 1e12, 6), "unit": "TFLOPS", "cores": threads, "kind": kind,
-            "sample": f"{len(cells)} cells ({'N=16, 80%, 4 OPT-66B shapes' if quick else 'full 48-cell sweep'})"
-                      f", first {rows} rows of each weight, one row-block shard per thread; "
-                      f"host: {cpu_model()}, {cpu_cores()} cores available",
-            "seconds": round(total_s, 2)}
+            "sample": cpu_sample_desc(nrows, threads, len(cells)), "seconds": round(total_s, 2), "steps": steps}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref), on this arm's workload sample, all host threads."""
     if rank != 0:
         return None
-    samples = []
-    for _ in range(args.warmup):
-        pass  # the reference has no warm state worth priming beyond the first call below
+    cells = cell_list(args)
+    weights = weight_list(cells)
+    threads = max(1, min(cpu_threads(), 64))
+    nrows = threads * CPU_ROWS_PER_THREAD
+
+    def gen(key):
+        m, k = SHAPES[key[0]]
+        return key, gen_random_sparse(m, k, key[1], SEED_W)[:nrows].copy()
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        head = dict(ex.map(gen, weights))
+    steps = max(1, min(args.steps, 3))
     t_start = time.perf_counter()
-    base = None
-    for i in range(max(1, args.ref_steps if args.ref_steps else min(args.steps, 3))):
-        base = cpu_baseline(args, quick=not args.ref_full)
-        samples.append(base["value"])
-    value = statistics.median(samples)
-    steps = len(samples)
+    base = cpu_baseline(head, cells, threads, steps=steps)
     ms = (time.perf_counter() - t_start) / steps * 1e3
-    base["value"] = value
+    value = base["value"]
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world,
             "steps": steps, "warmup": 0, "ms_per_step": round(ms, 1), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (fp16 inputs widened)",
-            "data": "reference gen_random_sparse inputs (seeded)",
-            "config": {"workload": WORKLOAD, "tile": "128x64 Tiled-CSL, bank-reordered",
-                       "sample": base["sample"]},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (fp16 inputs widened exactly, f32 accumulate)",
+            "data": "synthetic: the reference's gen_random_sparse bits (seeds 1 / 2)",
+            "config": bench_config(args, 1),
             "cpu_baseline": base,
             "e2e": {"value": value, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def main():
+    global SHAPES, WORKLOAD
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--suite", default="all", choices=sorted(SUITES),
+                    help="all = configs[1] + configs[3] (the metric's shapes); opt66b / opt175b = one of them")
     ap.add_argument("--only", default="", help="cells as shape:beta:n,... (e.g. ffn2:0.9:8)")
+    ap.add_argument("--split", type=int, default=0, help="force split-K S (0 = auto; SURVEY §8d C3)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--kernel-reps", type=int, default=5)
-    ap.add_argument("--ref-steps", type=int, default=0)
-    ap.add_argument("--ref-full", action="store_true")
-    ap.add_argument("--suite", default="opt66b", choices=["opt66b", "opt175b"],
-                    help="opt66b = BASELINE.json configs[1] (the metric's config); opt175b = SURVEY §8d C4")
-    ap.add_argument("--split", type=int, default=0, help="force split-K S (0 = auto; SURVEY §8d C3)")
+    ap.add_argument("--quick", action="store_true", help="headline only (no per-cell, e2e, cuBLAS, CPU legs)")
+    ap.add_argument("--kernel-reps", type=int, default=8)
     args = ap.parse_args()
-    if args.suite == "opt175b":
-        global SHAPES, WORKLOAD
-        SHAPES, WORKLOAD = SHAPES_175B, WORKLOAD_175B
+    SHAPES, WORKLOAD = SUITES[args.suite]
+    if args.only:
+        SHAPES = {**SHAPES_66B, **SHAPES_175B}
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
