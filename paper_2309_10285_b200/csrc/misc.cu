@@ -7,6 +7,9 @@
 //   gen_synthetic     <- bench inputs with gen_random_sparse's value law (matrix.cpp:56-63)
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
+#include "sm100_ptx.cuh"
 #include "tcsl_internal.cuh"
 
 namespace tcslk {
@@ -131,6 +134,7 @@ __global__ void __launch_bounds__(256) dense_gemm_exact_kernel(const uint16_t* _
 
 __global__ void splitk_reduce_kernel(const float* __restrict__ p, int split, size_t count,
                                      float* __restrict__ y) {
+  griddep_wait();  // launched with programmatic serialization: the partials come from the previous grid
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   if ((count & 3u) == 0) {
     const size_t c4 = count / 4;
@@ -159,6 +163,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ p, int split, siz
 __global__ void reduce_epilogue_kernel(const float* __restrict__ p, int split, size_t count, int n,
                                        const float* __restrict__ bias, int act, float* __restrict__ y32,
                                        uint16_t* __restrict__ y16) {
+  griddep_wait();
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
     float acc = p[i];
@@ -201,7 +206,27 @@ __global__ void gen_synthetic_kernel(uint16_t* __restrict__ w, uint64_t count, u
   }
 }
 
+// Launch with programmatic stream serialization (the kernel calls griddep_wait first).
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int blocks, int threads, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace
+
+bool pdl_enabled() {
+  static const bool on = !(getenv("TCSL_PDL") && atoi(getenv("TCSL_PDL")) == 0);
+  return on;
+}
 
 cudaError_t launch_decode(const uint32_t* off, const uint32_t* ent, uint64_t n_entries, uint32_t m,
                           uint32_t k, int m_tb, int k_tb, uint16_t* out, int* err, int strict, cudaStream_t s) {
@@ -245,8 +270,7 @@ cudaError_t launch_splitk_reduce(const float* p, int split, size_t count, float*
   if (count == 0) return cudaSuccess;
   const size_t work = (count & 3u) == 0 ? count / 4 : count;
   const int blocks = static_cast<int>(std::min<size_t>((work + 255) / 256, 148 * 8));
-  splitk_reduce_kernel<<<blocks, 256, 0, s>>>(p, split, count, y);
-  return cudaGetLastError();
+  return launch_pdl(splitk_reduce_kernel, blocks, 256, s, p, split, count, y);
 }
 
 cudaError_t launch_reduce_epilogue(const float* p, int split, uint32_t m, int n, const float* bias, int act,
@@ -254,8 +278,7 @@ cudaError_t launch_reduce_epilogue(const float* p, int split, uint32_t m, int n,
   const size_t count = static_cast<size_t>(m) * n;
   if (count == 0) return cudaSuccess;
   const int blocks = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 8));
-  reduce_epilogue_kernel<<<blocks, 256, 0, s>>>(p, split, count, n, bias, act, y32, y16);
-  return cudaGetLastError();
+  return launch_pdl(reduce_epilogue_kernel, blocks, 256, s, p, split, count, n, bias, act, y32, y16);
 }
 
 cudaError_t launch_rebase(const uint32_t* off, uint32_t t0, uint32_t t1, uint32_t* out, cudaStream_t s) {

@@ -69,7 +69,7 @@ constexpr int kGMax = 20;                      // groups per warp per tile remem
 // sparse tiles (<= 32 groups) are decoded by 8 teams of 2 warps with
 // clear-by-rescatter, dense ones (<= 81) by 8 teams of 3 warps with a zero
 // fill and 28 groups per warp in registers, denser ones by 6 teams of 4 warps.
-template <int T, int W, int G = (T % 2 == 0) ? 2 : 1, int KG = kGMax, bool ZF = false, int GA = G>
+template <int T, int W, int G = (T % 2 == 0) ? 2 : 1, int KG = kGMax, bool ZF = false>
 struct Teams {
   // KG: groups per warp per tile kept in registers; ZF: the team zero-fills the
   // whole 16 KB tile before each decode (no per-warp address memory) instead
@@ -85,12 +85,6 @@ struct Teams {
   static constexpr int kG = G;
   static_assert(kNA % kG == 0, "buffer groups");
   static constexpr int kNP = kNA / kG;
-  // "A full" is signalled per group of kGA consecutive buffers (the issuer waits
-  // once per group; each wait is a ~170-220-cycle round trip in the single issuing
-  // thread, profiles/r01_mma_loop_bench.txt), releases stay per kG.
-  static constexpr int kGA = GA;
-  static_assert(kNA % kGA == 0, "afull groups");
-  static constexpr int kNPA = kNA / kGA;
   static constexpr int kWarpEpi = T * W;           // 4 epilogue warps (id % 4 = TMEM lane quarter)
   static constexpr int kWarpStream = kWarpEpi + 4;  // entry stream: bulk copies only (blocking waits)
   static constexpr int kWarpX = kWarpStream + 1;   // X stages (TMA; blocking waits)
@@ -194,7 +188,6 @@ struct Params {
   int* err;
   unsigned long long* trace;  // TCSL_TRACE builds only: per-event clock64 stamps of CTA 0
   int dbg;                    // ablation switches (see DBG)
-  int v2opt;                  // v2 options: bit 0 = L2 prefetch of each published metadata batch's entries
 };
 
 #if defined(TCSL_TRACE) && defined(TCSL_HEARTBEAT)
@@ -212,7 +205,7 @@ __device__ unsigned* g_hb = nullptr;
 #endif
 // Ablation switches for performance experiments, TCSL_TRACE builds only (env
 // TCSL_DEBUG): 1 skip scatter+clear, 2 skip MMAs, 4 skip ring loads.
-#if defined(TCSL_TRACE) || defined(TCSL_PROF) || defined(TCSL_ABLATE)
+#if defined(TCSL_TRACE) || defined(TCSL_PROF)
 #define DBG(bit) (p.dbg & (bit))
 #else
 #define DBG(bit) 0
@@ -303,8 +296,6 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
   X(15) X(14) X(13) X(12) X(11) X(10) X(9) X(8) X(7) X(6) X(5) X(4) X(3) X(2) X(1) X(0)
 #define TCSL_DOWN20(X) X(19) X(18) X(17) X(16) TCSL_DOWN16(X)
 #define TCSL_DOWN28(X) X(27) X(26) X(25) X(24) X(23) X(22) X(21) X(20) TCSL_DOWN20(X)
-#define TCSL_DOWN40(X) \
-  X(39) X(38) X(37) X(36) X(35) X(34) X(33) X(32) X(31) X(30) X(29) X(28) TCSL_DOWN28(X)
 
 // Cases J >= KG are discarded at compile time (the count is clamped to KG).
 template <int KG>
@@ -433,9 +424,8 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   HB(4, gt);
   // s.ovf[b] = the last tile in buffer b for which some warp of the team wrote
   // more groups than it remembers: then the whole team zeroes the tile.
-  if (DBG(8)) {
-  } else if (TM::kZeroFill ? gt >= static_cast<uint32_t>(TM::kNA)
-                           : (gt >= static_cast<uint32_t>(TM::kNA) && lds32(s.ovf + 4 * b) == gt - TM::kNA)) {
+  if (TM::kZeroFill ? gt >= static_cast<uint32_t>(TM::kNA)
+                    : (gt >= static_cast<uint32_t>(TM::kNA) && lds32(s.ovf + 4 * b) == gt - TM::kNA)) {
     for (int r = tw; r < static_cast<int>(kABytes / 512); r += TM::kTeamWarps) sts128_zero(a_tile + 512 * r + 16 * lane);
   } else if (!TM::kZeroFill && !DBG(1)) {
     clear_groups<TM::kZeroFill ? 1 : KG>(Z, nz);
@@ -460,13 +450,13 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
     if (lane == 0) st_shared_u32(s.ovf + 4 * b, gt);
   }
   if (cnt > static_cast<uint32_t>(KG) && lane == 0) release_ring<RING / kChunk>(s, lo, hi);  // overflowed: read the ring until now
-  if (!DBG(32)) fence_proxy_async_smem();
+  fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
     // signal the MMA (an overflowed warp hands its ring bytes back only now)
     // a trailing group with fewer than TM::kG tiles: arrive for the missing ones too
-    const uint32_t ab = afull_leader + 8 * (b / TM::kGA);
-    const uint32_t missing = (gt % TM::kGA == 0 && gt + TM::kGA > total) ? gt + TM::kGA - total : 0u;
+    const uint32_t ab = afull_leader + 8 * (b / TM::kG);
+    const uint32_t missing = (gt % TM::kG == 0 && gt + TM::kG > total) ? gt + TM::kG - total : 0u;
     if (missing)
       asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0], %1;" ::"r"(ab), "r"(missing + 1) : "memory");
     else
@@ -491,8 +481,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
   const uint32_t sm = base + C::kOffSmall;
   s.cfull = opaque(sm);              // [kNB] ring chunk landed (bulk-copy bytes)
   s.cempty = s.cfull + 8 * kNB;      // [C::kNR] ring chunk consumed (decoders' complete_tx bytes)
-  s.afull = s.cempty + 8 * C::kNR;      // [TM::kNPA] even CTA: TM::kGA tiles x W decode warps x 2 CTAs arrivals
-  s.aempty = s.afull + 8 * TM::kNPA;     // [TM::kNP] both CTAs: MMA commit after the group's last tile
+  s.afull = s.cempty + 8 * C::kNR;      // [TM::kNP] even CTA: TM::kG tiles x 4 decode warps x 2 CTAs arrivals
+  s.aempty = s.afull + 8 * TM::kNP;      // [TM::kNP] both CTAs: MMA commit after the group's last tile
   s.xfull = s.aempty + 8 * TM::kNP;      // [NX] even CTA: 2 arrivals + both halves' bytes
   s.xempty = s.xfull + 8 * NX;       // [NX] both CTAs: MMA commit
   s.dfull = s.xempty + 8 * NX;       // [2] both CTAs: MMA commit
@@ -506,7 +496,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
   s.done = s.tiles_ready + 4;        // tiles whose metadata the decoders have read
   s.tab_ready = s.done + 4;          // unit table written (stream warp -> polling warp)
   s.tmem_slot = s.tab_ready + 4;
-  static_assert(8 * (kNB + C::kNR + TM::kNP + TM::kNPA + 2 * NX + 4 + kMeta) + 12 * kMaxUnits + 4 * TM::kNA + 16 <= kSmallBytes,
+  static_assert(8 * (kNB + C::kNR + 2 * TM::kNP + 2 * NX + 4 + kMeta) + 12 * kMaxUnits + 4 * TM::kNA + 16 <= kSmallBytes,
                 "small smem region");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (s.tmem_slot - base));
 
@@ -521,8 +511,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
     for (int i = 0; i < kNB; ++i) mbar_init(s.cfull + 8 * i, 1);
     for (int i = 0; i < C::kNR; ++i) mbar_init(s.cempty + 8 * i, 1);
     for (int i = 0; i < TM::kNA; ++i) {
-      if (i < TM::kNPA) mbar_init(s.afull + 8 * i, TM::kGA * 2 * TM::kTeamWarps);
-      if (i < TM::kNP) mbar_init(s.aempty + 8 * i, 1);
+      if (i < TM::kNP) {
+        mbar_init(s.afull + 8 * i, TM::kG * 2 * TM::kTeamWarps);
+        mbar_init(s.aempty + 8 * i, 1);
+      }
       st_shared_u32(s.ovf + 4 * i, 0xFFFFFFFFu);
     }
     for (int i = 0; i < NX; ++i) {
@@ -539,6 +531,15 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
     fence_barrier_init();
   }
   if (warp == TM::kWarpX && lane == 0) prefetch_tmap(&tmap_x);
+  if (warp == TM::kWarpMma) tmem_alloc_pair(s.tmem_slot, C::kTmemCols);
+  for (uint32_t i = threadIdx.x; i < TM::kNA * kABytes / 16; i += TM::kThreads) sts128_zero(s.a + 16 * i);
+  // Programmatic dependent launch: everything above touches only this CTA's smem,
+  // TMEM and parameters, so it overlaps the tail of the previous kernel in the
+  // stream; global memory is read and written only after the previous grid has
+  // completed. The next kernel may be scheduled at once (its CTAs start on the
+  // SMs this grid's CTAs leave).
+  griddep_wait();
+  griddep_launch_dependents();
   if (warp == TM::kWarpStream) {
     // Pull this CTA's tile offsets into L2 while the CTA initialises: the unit
     // validation and the metadata batches then read L2.
@@ -552,8 +553,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
       }
     }
   }
-  if (warp == TM::kWarpMma) tmem_alloc_pair(s.tmem_slot, C::kTmemCols);
-  for (uint32_t i = threadIdx.x; i < TM::kNA * kABytes / 16; i += TM::kThreads) sts128_zero(s.a + 16 * i);
   HB(60, 0);
   fence_proxy_async_smem();
   tc_fence_before();
@@ -895,7 +894,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
           const bool two = !quad && TM::kNA % 2 == 0 && (gt & 1) == 0 && kt + 1 < un.kt1 && in_stage + 1 < C::kTX;
           const uint32_t nt = quad ? 4u : (two ? 2u : 1u);
           TRACE(3, gt);
-          if (gt % TM::kGA == 0) mbar_wait(s.afull + 8 * (b / TM::kGA), (gt / TM::kNA) & 1);  // the group's tiles
+          if (gt % TM::kG == 0) mbar_wait(s.afull + 8 * (b / TM::kG), (gt / TM::kNA) & 1);  // the group's tiles
           PROF_ADD(2);
           TRACE(4, gt);
           tc_fence_after();
@@ -905,8 +904,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             if (j >= static_cast<int>(nt)) break;
-            if (j > 0 && (gt + j) % TM::kGA == 0) {
-              mbar_wait(s.afull + 8 * ((b + j) / TM::kGA), (gt / TM::kNA) & 1);
+            if (j > 0 && (gt + j) % TM::kG == 0) {
+              mbar_wait(s.afull + 8 * ((b + j) / TM::kG), (gt / TM::kNA) & 1);
               tc_fence_after();
             }
 #pragma unroll
@@ -949,541 +948,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
   tc_fence_before();
   cluster_sync_all();
   HB(51, 0);
-  if (warp == TM::kWarpMma) {
-    tc_fence_after();
-    tmem_dealloc_pair(tmem, C::kTmemCols);
-  }
-}
-
-// ============================================================================ K2 v2
-// Entries straight from HBM into the decode warps' registers (no smem ring).
-//
-// Round-1's K2 (above) streams every CTA's entries through a 64 KB shared-memory
-// ring with 16 KB bulk copies; decoders LDS their groups out of it. Measured on
-// B200 (profiles/r02_ncu_*): the ring costs two shared-memory wavefronts per
-// 32-entry group (the bulk write and the LDS) on a kernel whose shared-memory
-// pipe — not HBM — is the busiest unit, and a chunk is refilled only once every
-// tile that touches it has been consumed, which couples the teams' progress.
-// v2 removes the ring: each decode warp loads its share of a tile's groups with
-// coalesced 128-byte LDGs (one group per warp instruction, evict-first in L2),
-// issued right after it has scattered its previous tile, so the load latency
-// overlaps the wait for the tensor core to release the buffer. The 64 KB go to
-// four more dense-tile buffers (12), i.e. twelve tiles in flight per SM.
-// Further per-tile savings: +0.0 padding entries (value bits 0) are neither
-// scattered nor cleared (the buffer is zero there already), and the clear
-// addresses are kept packed two per register.
-template <int T, int W, int KG, bool ZF, int GA = 1>
-struct Teams2 {
-  static constexpr int kGK = KG;
-  static constexpr bool kZeroFill = ZF;
-  static constexpr int kTeams = T;
-  static constexpr int kTeamWarps = W;
-  static constexpr int kNA = T;  // one dense-tile buffer per team
-  static constexpr int kG = 1;   // aempty per tile
-  static constexpr int kNP = kNA;
-  static constexpr int kGA = GA;  // afull per group of kGA buffers (one issuer wait per group)
-  static_assert(kNA % kGA == 0, "afull groups");
-  static constexpr int kNPA = kNA / kGA;
-  static constexpr int kZP = ZF ? 1 : (KG + 1) / 2;  // packed clear addresses
-  static constexpr int kWarpEpi = T * W;
-  static constexpr int kWarpX = kWarpEpi + 4;
-  static constexpr int kWarpMeta = kWarpX + 1;  // offsets -> per-tile metadata, buffer releases, epilogue wake-ups
-  static constexpr int kWarpMma = kWarpMeta + 1;
-  static constexpr int kThreads = 32 * (kWarpMma + 1);
-  static constexpr int kBarEpi = 1 + T;
-  static_assert(kBarEpi + 2 <= 16, "named barriers");
-  static_assert(kThreads <= 1024, "threads");
-  static constexpr int kMaxRegs = ((16384 / (32 * ((kWarpMma + 1 + 3) / 4))) / 8) * 8;
-};
-
-constexpr uint32_t kSmall2 = 1024;  // barriers + metadata ring (see the kernel)
-
-template <int NH, int NA>
-struct Cfg2 : Cfg<NH, 1> {  // the X-stage / MMA constants of Cfg; its own smem map (no ring)
-  using B = Cfg<NH, 1>;
-  static constexpr uint32_t kOffSmall = 0;
-  static constexpr uint32_t kOffX = kSmall2;
-  static constexpr uint32_t kEndX = kOffX + B::kNX * B::kXStage;
-  static constexpr uint32_t kOffA = kEndX;
-  static constexpr uint32_t kSmem = kOffA + NA * kABytes;
-  static_assert(kSmem <= 227u * 1024u, "shared memory budget");
-};
-
-__device__ __forceinline__ uint32_t ldg_ef(const uint32_t* p, uint64_t pol) {
-  uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-
-// Element index (in halves) of tile location `loc` in the SWIZZLE_NONE K-major
-// core-matrix layout (a_addr without the base).
-__device__ __forceinline__ uint32_t elem_of(uint32_t loc) {
-  const uint32_t t = ((loc >> 3) ^ loc) & 0x38u;
-  return (loc ^ (t * 9u)) & 0x1FFFu;
-}
-
-// Issue the loads of this warp's groups (cnt clamped to KG): group J of the warp
-// is the 128-byte line g + J*32 entries past `src`; one lane per entry.
-template <int KG>
-__device__ __forceinline__ void ldg_groups(uint32_t (&E)[KG], const uint32_t* src, uint32_t cnt, uint64_t pol) {
-  switch (cnt) {
-#define TCSL_LG(J) \
-  case J + 1:      \
-    if constexpr ((J) < KG) E[(J) < KG ? (J) : 0] = ldg_ef(src + (J) * 32u, pol); [[fallthrough]];
-    default:
-      TCSL_DOWN40(TCSL_LG)
-    case 0:
-      break;
-#undef TCSL_LG
-  }
-}
-
-// Scatter with +0.0 padding skipped; REC: remember the written element indices
-// packed two per register (0xFFFF = nothing written) for clear-by-rescatter.
-template <int KG, int KZ, bool REC>
-__device__ __forceinline__ void scatter_groups2(const uint32_t (&E)[KG], uint32_t (&Z)[KZ], uint32_t cnt,
-                                                uint32_t a_tile) {
-  switch (cnt) {
-#define TCSL_SC2(J)                                                                  \
-  case J + 1:                                                                        \
-    if constexpr ((J) < KG) {                                                        \
-      const uint32_t e_ = E[(J) < KG ? (J) : 0];                                     \
-      const uint32_t w_ = elem_of(e_);                                               \
-      const bool v_ = (e_ >> 16) != 0;                                               \
-      sts16_if(a_tile + (w_ << 1), e_ >> 16, v_);                                    \
-      if constexpr (REC) {                                                           \
-        constexpr int zi_ = ((J) / 2) < KZ ? ((J) / 2) : 0;                          \
-        const uint32_t wz_ = v_ ? w_ : 0xFFFFu;                                      \
-        if constexpr ((J) & 1)                                                       \
-          Z[zi_] = (Z[zi_] & 0xFFFFu) | (wz_ << 16);                                 \
-        else                                                                         \
-          Z[zi_] = (Z[zi_] & 0xFFFF0000u) | wz_;                                     \
-      }                                                                              \
-    }                                                                                \
-    [[fallthrough]];
-    default:
-      TCSL_DOWN40(TCSL_SC2)
-    case 0:
-      break;
-#undef TCSL_SC2
-  }
-}
-
-template <int KZ>
-__device__ __forceinline__ void clear_groups2(const uint32_t (&Z)[KZ], uint32_t cnt, uint32_t a_tile) {
-  switch (cnt) {
-#define TCSL_CL2(J)                                                          \
-  case J + 1:                                                                \
-    if constexpr (((J) / 2) < KZ) {                                          \
-      const uint32_t w_ = (Z[(J) / 2 < KZ ? (J) / 2 : 0] >> (16 * ((J) & 1))) & 0xFFFFu; \
-      sts16_if(a_tile + (w_ << 1), 0u, w_ != 0xFFFFu);                       \
-    }                                                                        \
-    [[fallthrough]];
-    default:
-      TCSL_DOWN40(TCSL_CL2)
-    case 0:
-      break;
-#undef TCSL_CL2
-  }
-}
-
-struct Smem2 {
-  uint32_t a, x;
-  uint32_t afull, aempty, xfull, xempty, dfull, dempty;
-  uint32_t meta, ovf, tiles_ready, done, tmem_slot;
-};
-
-template <int NH, class TM>
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
-    spmm_v2_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
-  using C = Cfg2<NH, TM::kNA>;
-  constexpr int NX = C::kNX;
-  constexpr int KG = TM::kGK;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const uint32_t base = smem_u32(smem_raw);
-  Smem2 s;
-  s.x = opaque(base + C::kOffX);
-  s.a = opaque(base + C::kOffA);
-  const uint32_t sm = base + C::kOffSmall;
-  s.afull = opaque(sm);                   // [kNPA] even CTA: kGA tiles x 2 CTAs x W decode warps
-  s.aempty = s.afull + 8 * TM::kNPA;      // [kNA] both CTAs: MMA commit of the buffer's tile
-  s.xfull = s.aempty + 8 * TM::kNA;       // [NX] even CTA: 2 arrivals + both halves' bytes
-  s.xempty = s.xfull + 8 * NX;            // [NX] both CTAs: MMA commit
-  s.dfull = s.xempty + 8 * NX;            // [2] both CTAs: MMA commit
-  s.dempty = s.dfull + 16;                // [2] even CTA: 8 arrivals (4 epilogue warps x 2 CTAs)
-  s.meta = s.dempty + 16;                 // [kMeta] x (first entry, groups)
-  s.ovf = s.meta + 8 * kMeta;             // [kNA]
-  s.tiles_ready = s.ovf + 4 * TM::kNA;    // tiles with published metadata
-  s.done = s.tiles_ready + 4;             // tiles whose metadata every warp of its team has read
-  s.tmem_slot = s.done + 4;
-  static_assert(8 * (2 * TM::kNA + 2 * NX + 4 + kMeta) + 4 * TM::kNA + 12 <= kSmall2, "small smem region");
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (s.tmem_slot - base));
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const int cid = static_cast<int>(cluster_id_x());
-  const int ncl = static_cast<int>(num_clusters_x());
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < TM::kNA; ++i) {
-      if (i < TM::kNPA) mbar_init(s.afull + 8 * i, TM::kGA * 2 * TM::kTeamWarps);
-      mbar_init(s.aempty + 8 * i, 1);
-      st_shared_u32(s.ovf + 4 * i, 0xFFFFFFFFu);
-    }
-    for (int i = 0; i < NX; ++i) {
-      mbar_init(s.xfull + 8 * i, 2);
-      mbar_init(s.xempty + 8 * i, 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(s.dfull + 8 * i, 1);
-      mbar_init(s.dempty + 8 * i, 8);
-    }
-    st_shared_u32(s.tiles_ready, 0u);
-    st_shared_u32(s.done, 0u);
-    fence_barrier_init();
-  }
-  if (warp == TM::kWarpX && lane == 0) prefetch_tmap(&tmap_x);
-  if (warp == TM::kWarpMeta) {
-    // this CTA's tile offsets into L2 while the CTA initialises
-    for (int u = cid + lane * ncl; u < p.units; u += 32 * ncl) {
-      const Unit un = unit_of(p, u);
-      const int rb = 2 * un.rp + static_cast<int>(rank);
-      if (rb < p.tiles_m) {
-        const uint64_t b0 = reinterpret_cast<uint64_t>(p.off + static_cast<size_t>(rb) * p.tiles_k + un.kt0) & ~15ull;
-        const uint64_t b1 = (reinterpret_cast<uint64_t>(p.off + static_cast<size_t>(rb) * p.tiles_k + un.kt1 + 1) + 15) & ~15ull;
-        bulk_prefetch_l2(reinterpret_cast<const void*>(b0), static_cast<uint32_t>(b1 - b0));
-      }
-    }
-  }
-  if (warp == TM::kWarpMma) tmem_alloc_pair(s.tmem_slot, C::kTmemCols);
-  for (uint32_t i = threadIdx.x; i < TM::kNA * kABytes / 16; i += TM::kThreads) sts128_zero(s.a + 16 * i);
-  fence_proxy_async_smem();
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp < TM::kWarpEpi) {
-    // ---------------------------------------------------------------- decode teams
-    const int team = warp / TM::kTeamWarps;
-    const int tw = warp % TM::kTeamWarps;
-    uint32_t total = 0;
-    for (int u = cid; u < p.units; u += ncl) {
-      const Unit un = unit_of(p, u);
-      total += un.kt1 - un.kt0;
-    }
-    const uint32_t afull_leader = mapa_shared(s.afull, 0);
-    const uint64_t pol = policy_evict_first();
-    uint32_t E[KG];
-#pragma unroll
-    for (int j = 0; j < KG; ++j) E[j] = 0u;
-    uint32_t Z[TM::kZP];
-#pragma unroll
-    for (int j = 0; j < TM::kZP; ++j) Z[j] = 0xFFFFFFFFu;
-    uint32_t err_or = 0, nz = 0;
-    const uint32_t b = static_cast<uint32_t>(team);
-    const uint32_t a_tile = s.a + b * kABytes;
-    // this warp's part of tile gt: metadata -> [first entry, count) -> loads issued
-    auto fetch = [&](uint32_t gt, uint32_t& g_first, uint32_t& cnt) {
-      if (ld_acquire_u32(s.tiles_ready) <= gt) {
-        const long long t0 = clock64();
-        while (ld_acquire_u32(s.tiles_ready) <= gt) {
-          __nanosleep(32);
-          if (clock64() - t0 > 40000000000LL) __trap();
-        }
-      }
-      const uint2 meta = lds64(s.meta + 8 * (gt % kMeta));  // (first entry, groups)
-      const uint32_t g0w = meta.y * tw / TM::kTeamWarps, g1w = meta.y * (tw + 1) / TM::kTeamWarps;
-      cnt = g1w - g0w;
-      g_first = meta.x + g0w * 32u;
-      ldg_groups(E, p.ent + g_first + lane, min(cnt, static_cast<uint32_t>(KG)), pol);
-    };
-    uint32_t g_first = 0, cnt = 0;
-    uint32_t gt = static_cast<uint32_t>(team);
-    if (gt < total) fetch(gt, g_first, cnt);
-    for (; gt < total; gt += TM::kTeams) {
-      const uint32_t ncnt = min(cnt, static_cast<uint32_t>(KG));
-      // buffer free again: the MMA of tile gt - kTeams has completed (the meta
-      // warp saw the commit and arrives on the team's named barrier)
-      if (gt >= static_cast<uint32_t>(TM::kTeams)) named_bar_sync(1 + team, (TM::kTeamWarps + 1) * 32);
-      if (TM::kZeroFill ? gt >= static_cast<uint32_t>(TM::kNA)
-                        : (gt >= static_cast<uint32_t>(TM::kNA) && lds32(s.ovf + 4 * b) == gt - TM::kNA)) {
-        for (int r = tw; r < static_cast<int>(kABytes / 512); r += TM::kTeamWarps) sts128_zero(a_tile + 512 * r + 16 * lane);
-      } else if (!TM::kZeroFill) {
-        clear_groups2<TM::kZP>(Z, nz, a_tile);
-      }
-      named_bar_sync(1 + team, TM::kTeamWarps * 32);
-      if (tw == 0 && lane == 0)
-        asm volatile("red.relaxed.cta.shared::cta.add.u32 [%0], 1;" ::"r"(s.done) : "memory");  // meta slot read
-#pragma unroll
-      for (int j = 0; j < KG; ++j) err_or |= E[j];
-      scatter_groups2<KG, TM::kZP, !TM::kZeroFill>(E, Z, ncnt, a_tile);
-      nz = ncnt;
-      if (cnt > static_cast<uint32_t>(KG)) {  // more groups than registers: straight from L2/HBM
-        for (uint32_t g = KG; g < cnt; ++g) {
-          const uint32_t e = ldg_ef(p.ent + g_first + g * 32u + lane, pol);
-          err_or |= e;
-          sts16_if(a_addr(a_tile, e), e >> 16, (e >> 16) != 0);
-        }
-        if (lane == 0) st_shared_u32(s.ovf + 4 * b, gt);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        // a trailing group with fewer than kGA tiles: arrive for the missing ones too
-        const uint32_t ab = afull_leader + 8 * (b / TM::kGA);
-        const uint32_t missing = (gt % TM::kGA == 0 && gt + TM::kGA > total) ? gt + TM::kGA - total : 0u;
-        if (missing)
-          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0], %1;" ::"r"(ab), "r"(missing + 1) : "memory");
-        else
-          mbar_arrive_cluster(ab);
-      }
-      // next tile of this team: its loads fly while the MMA of this one runs
-      if (gt + TM::kTeams < total) fetch(gt + TM::kTeams, g_first, cnt);
-    }
-    if (__any_sync(0xffffffffu, (err_or & 0xE000u) != 0) && lane == 0)
-      raise_dev(p.err, TCSL_STATUS_LOCATION_OUT_OF_RANGE);
-  } else if (warp < TM::kWarpEpi + 4) {
-    // ---------------------------------------------------------------- epilogue (as v1)
-    const int q = warp & 3;
-    const uint32_t dempty_leader = mapa_shared(s.dempty, 0);
-    uint32_t ui = 0;
-    for (int u = cid; u < p.units; u += ncl, ++ui) {
-      const Unit un = unit_of(p, u);
-      const uint32_t acc = ui & 1;
-      named_bar_sync(TM::kBarEpi + acc, 5 * 32);
-      tc_fence_after();
-      const int rb = 2 * un.rp + static_cast<int>(rank);
-      const long long row = static_cast<long long>(rb) * kMTB + q * 32 + lane;
-      if (rb < p.tiles_m) {
-        float* dst =
-            p.out + (p.split > 1 ? static_cast<long long>(un.s) * p.m * p.ldo : 0ll) + row * p.ldo + p.col0;
-        const bool row_ok = row < p.m;
-        const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * C::kN;
-        const int ncol = min(C::kN, p.n - p.col0);
-        const bool fused = p.bias != nullptr || p.act != 0 || p.out_f16;
-        const float b_row = (p.bias != nullptr && row_ok) ? __ldg(p.bias + row) : 0.0f;
-#pragma unroll
-        for (int c0 = 0; c0 < C::kN; c0 += 16) {
-          uint32_t r[16];
-          tmem_ld16(t_base + c0, r);
-          tmem_ld_wait();
-          if (row_ok && fused) {
-            float v[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = epilogue_value(__uint_as_float(r[j]), b_row, p.act);
-            if (p.out_f16) {
-              uint16_t* d16 = p.out16 + row * p.ldo + p.col0 + c0;
-              if (c0 + 16 <= ncol && ((reinterpret_cast<uintptr_t>(d16) & 15u) == 0)) {
-                uint32_t h[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) h[j] = f16_bits_rne(v[2 * j]) | (f16_bits_rne(v[2 * j + 1]) << 16);
-                reinterpret_cast<uint4*>(d16)[0] = make_uint4(h[0], h[1], h[2], h[3]);
-                reinterpret_cast<uint4*>(d16)[1] = make_uint4(h[4], h[5], h[6], h[7]);
-              } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                  if (c0 + j < ncol) d16[j] = static_cast<uint16_t>(f16_bits_rne(v[j]));
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (c0 + j < ncol) dst[c0 + j] = v[j];
-            }
-          } else if (row_ok) {
-            if (c0 + 16 <= ncol && ((reinterpret_cast<uintptr_t>(dst + c0) & 15u) == 0)) {
-              float4* d4 = reinterpret_cast<float4*>(dst + c0);
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                    __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (c0 + j < ncol) dst[c0 + j] = __uint_as_float(r[j]);
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(dempty_leader + 8 * acc);
-    }
-  } else if (warp == TM::kWarpX) {
-    // ---------------------------------------------------------------- X stages (as v1)
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_last();
-      const uint32_t xfull_leader = mapa_shared(s.xfull, 0);
-      uint32_t gs = 0;
-      for (int u = cid; u < p.units; u += ncl) {
-        const Unit un = unit_of(p, u);
-        for (int kt = un.kt0; kt < un.kt1; kt += C::kTX, ++gs) {
-          const uint32_t slot = gs % NX;
-          if (gs >= static_cast<uint32_t>(NX)) mbar_wait(s.xempty + 8 * slot, ((gs / NX) - 1) & 1);
-          mbar_arrive_expect_tx_cluster(xfull_leader + 8 * slot, C::kXStage);
-#pragma unroll
-          for (int bx = 0; bx < C::kBoxes; ++bx)
-            tma_load_2d_pair(s.x + slot * C::kXStage + bx * C::kBoxBytes, &tmap_x,
-                             p.col0 + static_cast<int>(rank) * NH + bx * C::kBoxW, kt * kKTB, xfull_leader + 8 * slot,
-                             pol);
-        }
-      }
-    }
-  } else if (warp == TM::kWarpMeta) {
-    // ---------------------------------------------------------------- metadata warp
-    // (a) per-tile metadata (first entry, groups), 32 tiles per step, one lane per
-    //     tile, offsets loaded one step ahead; each tile's offsets are validated
-    //     (span inside [0, E], whole 32-entry groups): an invalid tile decodes as
-    //     empty and raises inconsistent_offsets; (b) buffer releases; (c) epilogue
-    //     wake-ups. Non-blocking mbarrier tests only.
-    uint32_t nunits = 0, ntiles = 0;
-    for (int u = cid; u < p.units; u += ncl, ++nunits) {
-      const Unit un = unit_of(p, u);
-      ntiles += un.kt1 - un.kt0;
-    }
-    uint32_t gt = 0, mkt = 0;
-    int mu_id = cid;
-    uint32_t pend = 0, pa0 = 0, pa1 = 0;
-    bool real = false;
-    uint32_t eu = 0, rel = 0;
-    auto prefetch_batch = [&]() {
-      const Unit un = unit_of(p, mu_id);
-      const int rb = 2 * un.rp + static_cast<int>(rank);
-      pend = min(32u, static_cast<uint32_t>(un.kt1 - un.kt0) - mkt);
-      real = rb < p.tiles_m;
-      pa0 = pa1 = 0;
-      if (real && lane < pend) {
-        const uint32_t t = static_cast<uint32_t>(rb) * p.tiles_k + un.kt0 + mkt + lane;
-        pa0 = __ldg(p.off + t);
-        pa1 = __ldg(p.off + t + 1);
-      }
-    };
-    if (ntiles) prefetch_batch();
-    long long idle_t0 = clock64();
-    while (gt < ntiles || eu < nunits || rel < ntiles) {
-      bool progress = false;
-      while (rel < ntiles &&
-             __shfl_sync(0xffffffffu, mbar_test_wait(s.aempty + 8 * (rel % TM::kNA), (rel / TM::kNA) & 1) ? 1 : 0, 0)) {
-        if (rel + TM::kNA < ntiles)
-          asm volatile("bar.arrive %0, %1;" ::"r"(1 + (rel % TM::kNA)), "r"((TM::kTeamWarps + 1) * 32) : "memory");
-        ++rel;
-        progress = true;
-      }
-      while (eu < nunits && __shfl_sync(0xffffffffu, mbar_test_wait(s.dfull + 8 * (eu & 1), (eu >> 1) & 1) ? 1 : 0, 0)) {
-        asm volatile("bar.arrive %0, %1;" ::"r"(TM::kBarEpi + (eu & 1)), "r"(5 * 32) : "memory");
-        ++eu;
-        progress = true;
-      }
-      if (pend) {
-        const uint32_t room = __shfl_sync(0xffffffffu, ld_acquire_u32(s.done), 0) + (kMeta - 16);
-        if (gt + pend <= room) {
-          if (lane < pend) {
-            uint32_t ng = 0;
-            if (real) {
-              const bool bad = pa1 < pa0 || pa1 > p.n_entries || ((pa1 - pa0) & 31u) != 0 || (pa0 & 31u) != 0;
-              if (bad)
-                raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
-              else
-                ng = (pa1 - pa0) >> 5;
-            }
-            st_shared_v2(s.meta + 8 * ((gt + lane) % kMeta), pa0, ng);
-          }
-          __threadfence_block();
-          __syncwarp();
-          if ((p.v2opt & 1) && real) {
-            // the batch's entries are contiguous: pull them into L2 now, so the decoders'
-            // loads (issued one team cycle later) hit L2 instead of waiting on HBM
-            const uint32_t e0 = __shfl_sync(0xffffffffu, pa0, 0), e1 = __shfl_sync(0xffffffffu, pa1, pend - 1);
-            if (lane == 0 && e1 > e0 && e1 <= p.n_entries && ((e0 | e1) & 3u) == 0) {
-              const char* src = reinterpret_cast<const char*>(p.ent + e0);
-              const uint32_t bytes = (e1 - e0) * 4u;
-              for (uint32_t o = 0; o < bytes; o += 65536u)
-                bulk_prefetch_l2(src + o, min(65536u, bytes - o));
-            }
-          }
-          gt += pend;
-          mkt += pend;
-          const Unit un = unit_of(p, mu_id);
-          if (mkt == static_cast<uint32_t>(un.kt1 - un.kt0)) {
-            mkt = 0;
-            mu_id += ncl;
-          }
-          pend = 0;
-          if (lane == 0) st_release_u32(s.tiles_ready, gt);
-          if (gt < ntiles) prefetch_batch();
-          progress = true;
-        }
-      }
-      if (progress) {
-        idle_t0 = clock64();
-      } else {
-        __nanosleep(64);
-        if (clock64() - idle_t0 > 40000000000LL) __trap();
-      }
-    }
-  } else if (warp == TM::kWarpMma && rank == 0) {
-    // ---------------------------------------------------------------- MMA issuer (as v1, per-tile buffers)
-    const uint64_t a_desc0 = smem_desc(s.a, 128, 1024, 0);
-    const uint64_t b_desc0 = smem_desc(s.x, C::kLBO, C::kSBO, C::kLayout);
-    uint32_t total = 0;
-    for (int u = cid; u < p.units; u += ncl) {
-      const Unit un = unit_of(p, u);
-      total += un.kt1 - un.kt0;
-    }
-    if (elect_one()) {
-      uint32_t gt = 0, ui = 0, gs = 0;
-      for (int u = cid; u < p.units; u += ncl, ++ui) {
-        const Unit un = unit_of(p, u);
-        const uint32_t acc = ui & 1;
-        if (ui >= 2) mbar_wait(s.dempty + 8 * acc, ((ui >> 1) - 1) & 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem + acc * C::kN;
-        int in_stage = 0;
-        for (int kt = un.kt0; kt < un.kt1;) {
-          const uint32_t xs = gs % NX;
-          if (in_stage == 0) mbar_wait(s.xfull + 8 * xs, (gs / NX) & 1);
-          const uint32_t b = gt % TM::kNA;
-          // a whole 4-tile X stage per iteration when its tiles sit in consecutive buffers
-          const bool quad = C::kTX == 4 && TM::kNA % 4 == 0 && (gt & 3) == 0 && in_stage == 0 && kt + 3 < un.kt1 &&
-                            b + 3 < static_cast<uint32_t>(TM::kNA);
-          const bool two = !quad && b + 1 < static_cast<uint32_t>(TM::kNA) && kt + 1 < un.kt1 && in_stage + 1 < C::kTX;
-          const uint32_t nt = quad ? 4u : (two ? 2u : 1u);
-          const uint64_t ad = a_desc0 + ((b * kABytes) >> 4);
-          const uint64_t bd = b_desc0 + ((xs * C::kXStage + in_stage * C::kTileStep) >> 4);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (j >= static_cast<int>(nt)) break;
-            if ((gt + j) % TM::kGA == 0) {
-              mbar_wait(s.afull + 8 * ((b + j) / TM::kGA), (gt / TM::kNA) & 1);
-              tc_fence_after();
-            }
-#pragma unroll
-            for (int k4 = 0; k4 < kKTB / 16; ++k4)
-              mma_f16_ss_pair(d_tmem, ad + ((j * kABytes + k4 * 256) >> 4),
-                              bd + ((j * C::kTileStep + k4 * C::kKStep) >> 4), C::kIdesc,
-                              (kt > un.kt0 || j > 0 || k4 > 0) ? 1u : 0u);
-            mma_commit_pair(s.aempty + 8 * (b + j), 3);
-          }
-          if (in_stage + static_cast<int>(nt) == C::kTX || kt + static_cast<int>(nt) == un.kt1) {
-            mma_commit_pair(s.xempty + 8 * xs, 3);
-            ++gs;
-            in_stage = 0;
-          } else {
-            in_stage += nt;
-          }
-          kt += nt;
-          gt += nt;
-        }
-        mma_commit_pair(s.dfull + 8 * acc, 3);
-      }
-    }
-    __syncwarp();
-  }
-
-  __syncwarp();
-  tc_fence_before();
-  cluster_sync_all();
   if (warp == TM::kWarpMma) {
     tc_fence_after();
     tmem_dealloc_pair(tmem, C::kTmemCols);
@@ -1584,8 +1048,17 @@ cudaError_t launch_shape(const Params& p, const CUtensorMap& tm, int clusters, c
   if (e != cudaSuccess) return e;
   const int nc = std::min(clusters, mc);
   if ((p.units + nc - 1) / nc > kMaxUnits) return cudaErrorInvalidConfiguration;  // unit table size
-  spmm_sm100_kernel<NH, TM><<<2 * nc, TM::kThreads, C::kSmem, s>>>(tm, p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * nc, 1, 1);
+  cfg.blockDim = dim3(TM::kThreads, 1, 1);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, spmm_sm100_kernel<NH, TM>, tm, p);
 }
 
 // Team shape for a matrix: 2-warp teams while a warp's share of a mean tile
@@ -1600,90 +1073,14 @@ bool dense3_teams(uint64_t n_entries, uint64_t tiles) {
   return mean_groups(n_entries, tiles) <= 0.97 * TeamsDense3::kGK * TeamsDense3::kTeamWarps;
 }
 
-int ga_env() {
-  static const int ga = getenv("TCSL_GA") ? atoi(getenv("TCSL_GA")) : 4;
-  return ga;
-}
-
 template <int NH>
 cudaError_t launch_nh(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
   const uint64_t tiles = static_cast<uint64_t>(p.tiles_m) * p.tiles_k;
-  const bool ga4 = ga_env() == 4;
   if (sparse_teams(p.n_entries, tiles)) {
-    return ga4 ? launch_shape<NH, Teams<8, 2, 1, kGMax, false, 4>>(p, tm, clusters, s)
-               : launch_shape<NH, TeamsSparse>(p, tm, clusters, s);
+    return launch_shape<NH, TeamsSparse>(p, tm, clusters, s);
   }
-  if (dense3_teams(p.n_entries, tiles))
-    return ga4 ? launch_shape<NH, Teams<8, 3, 1, 28, true, 4>>(p, tm, clusters, s)
-               : launch_shape<NH, TeamsDense3>(p, tm, clusters, s);
+  if (dense3_teams(p.n_entries, tiles)) return launch_shape<NH, TeamsDense3>(p, tm, clusters, s);
   return launch_shape<NH, TeamsDense>(p, tm, clusters, s);
-}
-
-// ---- v2 launch
-using Teams2Sparse = Teams2<12, 2, 20, false>;  // <= 32 groups per tile (beta >~ 0.87): clear-by-rescatter
-using Teams2Mid = Teams2<12, 2, 28, true>;      // <= 56 (beta ~0.78-0.87): zero fill, 28 groups per warp in registers
-using Teams2Dense = Teams2<12, 2, 40, true>;    // denser: zero fill, 40 groups per warp in registers
-
-template <int NH, class TM>
-int max_clusters2(cudaError_t* e) {
-  static std::atomic<int> cache[kMaxDevices];
-  const int dev = current_device();
-  int cached = cache[dev].load(std::memory_order_acquire);
-  if (!cached) {
-    using C = Cfg2<NH, TM::kNA>;
-    *e = cudaFuncSetAttribute(spmm_v2_kernel<NH, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(C::kSmem));
-    if (*e != cudaSuccess) return 0;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * 74, 1, 1);
-    cfg.blockDim = dim3(TM::kThreads, 1, 1);
-    cfg.dynamicSmemBytes = C::kSmem;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int nc = 0;
-    if (cudaOccupancyMaxActiveClusters(&nc, spmm_v2_kernel<NH, TM>, &cfg) != cudaSuccess || nc <= 0) {
-      cudaGetLastError();
-      nc = num_sms() / 2;
-    }
-    cached = nc;
-    cache[dev].store(nc, std::memory_order_release);
-  }
-  return cached;
-}
-
-template <int NH, class TM>
-cudaError_t launch_shape2(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
-  using C = Cfg2<NH, TM::kNA>;
-  cudaError_t e = cudaSuccess;
-  const int mc = max_clusters2<NH, TM>(&e);
-  if (e != cudaSuccess) return e;
-  const int nc = std::min(clusters, mc);
-  spmm_v2_kernel<NH, TM><<<2 * nc, TM::kThreads, C::kSmem, s>>>(tm, p);
-  return cudaGetLastError();
-}
-
-template <int NH>
-cudaError_t launch_nh2(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
-  const double g = mean_groups(p.n_entries, static_cast<uint64_t>(p.tiles_m) * p.tiles_k);
-  const bool ga4 = ga_env() == 4;
-  if (g <= 0.8 * 2 * 20)
-    return ga4 ? launch_shape2<NH, Teams2<12, 2, 20, false, 4>>(p, tm, clusters, s)
-               : launch_shape2<NH, Teams2Sparse>(p, tm, clusters, s);
-  if (g <= 0.97 * 2 * 28)
-    return ga4 ? launch_shape2<NH, Teams2<12, 2, 28, true, 4>>(p, tm, clusters, s)
-               : launch_shape2<NH, Teams2Mid>(p, tm, clusters, s);
-  return ga4 ? launch_shape2<NH, Teams2<12, 2, 40, true, 4>>(p, tm, clusters, s)
-             : launch_shape2<NH, Teams2Dense>(p, tm, clusters, s);
-}
-
-bool use_v1() {
-  static const bool v1 = getenv("TCSL_K2_V1") != nullptr && atoi(getenv("TCSL_K2_V1")) != 0;
-  return v1;
 }
 
 }  // namespace
@@ -1709,7 +1106,9 @@ int auto_split(uint32_t m, uint32_t k, int n, double avg_entries_per_tile) {
   const int tiles_mp = (tiles_m + 1) / 2;
   const int clusters = num_sms() / 2;
   // per-SM streaming rate ~ 6.5 TB/s / 148; MMA floor ~0.05 us per tile (CTA pair)
-  const double t_tile = std::max(avg_entries_per_tile * 4.0 / 44.0e3, 0.05);
+  // measured cost of one tile pair per cluster, ~0.23-0.34 us at beta 0.9-0.7 (profiles/r02_bench_*);
+  // the entry-byte term keeps denser inputs proportional
+  const double t_tile = std::max(avg_entries_per_tile * 4.0 / 44.0e3, 0.25);
   const double mn_bytes = static_cast<double>(m) * std::min(n, 256) * 4.0;
   int best = 1;
   double best_cost = split_cost(tiles_mp, tiles_k, 1, clusters, t_tile, mn_bytes);
@@ -1769,8 +1168,6 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
   p.trace = g_trace;
   static const int dbg_env = getenv("TCSL_DEBUG") ? atoi(getenv("TCSL_DEBUG")) : 0;
   p.dbg = dbg_env;
-  static const int v2opt_env = getenv("TCSL_V2OPT") ? atoi(getenv("TCSL_V2OPT")) : 1;
-  p.v2opt = v2opt_env;
   // Column slabs of <= 256 (one TMEM accumulator pair each).
   for (int col0 = 0; col0 < plan.n; col0 += 256) {
     const int nh = half_n(std::min(256, plan.n - col0));
@@ -1792,22 +1189,12 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     cudaError_t e;
-    if (use_v1()) {
-      switch (nh) {
-        case 8: e = launch_nh<8>(p, tm, plan.grid, s); break;
-        case 16: e = launch_nh<16>(p, tm, plan.grid, s); break;
-        case 32: e = launch_nh<32>(p, tm, plan.grid, s); break;
-        case 64: e = launch_nh<64>(p, tm, plan.grid, s); break;
-        default: e = launch_nh<128>(p, tm, plan.grid, s); break;
-      }
-    } else {
-      switch (nh) {
-        case 8: e = launch_nh2<8>(p, tm, plan.grid, s); break;
-        case 16: e = launch_nh2<16>(p, tm, plan.grid, s); break;
-        case 32: e = launch_nh2<32>(p, tm, plan.grid, s); break;
-        case 64: e = launch_nh2<64>(p, tm, plan.grid, s); break;
-        default: e = launch_nh2<128>(p, tm, plan.grid, s); break;
-      }
+    switch (nh) {
+      case 8: e = launch_nh<8>(p, tm, plan.grid, s); break;
+      case 16: e = launch_nh<16>(p, tm, plan.grid, s); break;
+      case 32: e = launch_nh<32>(p, tm, plan.grid, s); break;
+      case 64: e = launch_nh<64>(p, tm, plan.grid, s); break;
+      default: e = launch_nh<128>(p, tm, plan.grid, s); break;
     }
     if (e != cudaSuccess) return e;
   }

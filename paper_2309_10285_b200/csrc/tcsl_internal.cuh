@@ -33,6 +33,9 @@ constexpr uint32_t kFlagFringePayload = TCSL_FLAG_FRINGE_PAYLOAD;
 
 inline int div_up_i(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
 
+// Programmatic dependent launch for the SpMM-path kernels (env TCSL_PDL=0 turns it off).
+bool pdl_enabled();
+
 // binary16 bits of v, round to nearest even, overflow to +-inf, every NaN the
 // canonical quiet NaN 0x7E00: f16_from_f32 (proj/src/half.cpp:10-40).
 __device__ __forceinline__ uint32_t f16_bits_rne(float v) {
