@@ -89,24 +89,34 @@ struct Teams {
   static constexpr int kWarpStream = kWarpEpi + 4;  // entry stream: bulk copies only (blocking waits)
   static constexpr int kWarpX = kWarpStream + 1;   // X stages (TMA; blocking waits)
   static constexpr int kWarpPoll = kWarpX + 1;     // polling warp: tile metadata, wake-ups (no TMA)
-  static constexpr int kWarpMma = kWarpPoll + 1;
-  static constexpr int kThreads = 32 * (kWarpMma + 1);
+  static constexpr int kWarpMma = kWarpPoll + 1;   // TMEM owner; MMA issuer 0 (+ issuers 1 .. I-1 above it)
   // Named barrier 1 + t serves team t twice per tile: the buffer-release wake-up
   // (W warps + the polling warp, which arrives once the MMA of the buffer's
   // previous tile has committed) and then the team barrier (W warps). The next
   // release can only follow that tile's MMA, i.e. after the team barrier phase.
   static constexpr int kBarEpi = 1 + T;            // 2 epilogue wake-ups (per accumulator)
   static_assert(kBarEpi + 2 <= 16, "named barriers");
+};
+// Warp budget of a team shape with I MMA-issuer warps (even CTA: issuer i owns the
+// X stages gs = i (mod I) and accumulates into its own TMEM accumulator; the
+// epilogue sums the I partial accumulators).
+template <class TM, int I>
+struct Roles {
+  static constexpr int kIss = I;
+  static constexpr int kWarps = TM::kWarpMma + I;
+  static constexpr int kThreads = 32 * kWarps;
   // Register file per SMSP: ceil(warps / 4) * 32 * regs <= 16384.
-  static constexpr int kMaxRegs = ((16384 / (32 * ((kWarpMma + 1 + 3) / 4))) / 8) * 8;
+  static constexpr int kMaxRegs = ((16384 / (32 * ((kWarps + 3) / 4))) / 8) * 8;
 };
 #ifndef TCSL_SPARSE_G
 #define TCSL_SPARSE_G 1
 #endif
-#ifndef TCSL_QUAD
-#define TCSL_QUAD 1
+#ifndef TCSL_POLL_RELEASE
+#define TCSL_POLL_RELEASE 0
 #endif
-constexpr bool kQuad = TCSL_QUAD;  // issue a whole 4-tile X stage per MMA-loop iteration
+// Buffer release through the polling warp (named barrier) instead of each team
+// waiting on aempty itself (A/B builds only).
+constexpr bool kPollRelease = TCSL_POLL_RELEASE;
 using TeamsSparse = Teams<8, 2, TCSL_SPARSE_G>;  // G=1, per-tile release: +2-5 % over G=2 (r01_ablation_mma_loop)
 #ifndef TCSL_DENSE_T
 #define TCSL_DENSE_T 6
@@ -135,7 +145,7 @@ constexpr int kMeta = 64;                      // per-tile metadata ring (stream
 constexpr uint32_t kSmallBytes = 3072;         // barriers + tables (see Smem)
 
 // NH = B columns held by each CTA of the pair (the MMA's N is 2 * NH).
-template <int NH, int NA>
+template <int NH, int NA, int I = 1>
 struct Cfg {
   static constexpr int kN = 2 * NH;
   static constexpr int kBoxW = NH < 64 ? NH : 64;  // TMA box / swizzle atom width
@@ -152,8 +162,11 @@ struct Cfg {
   static constexpr uint32_t kSBO = kRowBytes == 16 ? 128u : 8u * kRowBytes;
   static constexpr uint32_t kKStep = 16u * kRowBytes;     // 16 k-rows per MMA
   static constexpr uint32_t kTileStep = 64u * kRowBytes;  // next k-tile inside a stage
+  // I issuers x 2 accumulators (double-buffered across units) x kN columns
+  static constexpr int kAccCols = 2 * I * kN;
+  static_assert(kAccCols <= 512, "TMEM columns");
   static constexpr uint32_t kTmemCols =
-      (2 * kN) <= 32 ? 32 : ((2 * kN) <= 64 ? 64 : ((2 * kN) <= 128 ? 128 : ((2 * kN) <= 256 ? 256 : 512)));
+      kAccCols <= 32 ? 32 : (kAccCols <= 64 ? 64 : (kAccCols <= 128 ? 128 : (kAccCols <= 256 ? 256 : 512)));
   static constexpr uint32_t kIdesc = idesc_f16_f32(256, kN, 1);
   // smem, relative to the dynamic-smem base B (1 KB past the 16 KB-aligned window
   // start on sm_100: the driver reserves the first 1 KB): entry ring, small
@@ -216,8 +229,13 @@ __device__ unsigned* g_hb = nullptr;
 #else
 #define TRACE(slot, idx) do { } while (0)
 #endif
-#if defined(TCSL_TRACE) || defined(TCSL_PROF)
+// Per-warp cycle accounting (clock64 around every phase) is heavy: TCSL_PROF
+// builds only, so TCSL_TRACE timelines stay close to the product kernel's timing.
+#if defined(TCSL_PROF)
 #define TCSL_PROFILING 1
+#endif
+#if defined(TCSL_TRACE) || defined(TCSL_PROF)
+#define TCSL_DEBUG_HOOKS 1
 #endif
 // Per-warp cycle accounting of CTA 0 (profiling builds, tools/prof_spmm.py),
 // dumped to trace slot 15. Empty in product builds.
@@ -239,6 +257,12 @@ struct Prof {
 #define PROF_ADD(i) do { } while (0)
 #define PROF_DUMP(base, n) do { } while (0)
 #endif
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct Unit {
   int rp, s, kt0, kt1;
@@ -382,6 +406,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
     }
   }
   const uint2 meta = lds64(s.meta + 8 * (gt % kMeta));  // (stream offset, groups)
+  if (tw == 0 && lane == 0) TRACE(11, gt);
   PROF_ADD(0);
   const uint32_t g0w = meta.y * tw / TM::kTeamWarps, g1w = meta.y * (tw + 1) / TM::kTeamWarps;
   const uint32_t cnt = g1w - g0w;
@@ -391,6 +416,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   if (cnt) {
     for (uint32_t k = lo / kChunk; k <= (hi - 1) / kChunk; ++k)
       mbar_wait_backoff(s.cfull + 8 * (k % kNB), (k / kNB) & 1, 64);
+    if (tw == 0 && lane == 0) TRACE(12, gt);
     PROF_ADD(1);
     if (DBG(4)) {
     } else if ((lo & (RING - 1)) + cnt * 128u <= RING) {
@@ -415,10 +441,16 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   const uint32_t b = gt % TM::kNA;
   const uint32_t a_tile = s.a + b * kABytes;
   HB(3, gt);
-  // buffer b free again: the MMA of tile gt - TM::kNA has completed. The polling
-  // warp observed that commit and arrives here; waiting on a named barrier
-  // costs no issue slots and no sync-unit polling.
+  // buffer b free again: the MMA of tile gt - TM::kNA has completed (its commit
+  // arrives on aempty[b] in both CTAs). Every warp of the team waits on the
+  // mbarrier itself: a hop through the polling warp costs ~1000 cycles of the
+  // buffer cycle (profiles/r02_trace_*). No parity aliasing: the next phase
+  // needs this team's next tile in the buffer.
+#if TCSL_POLL_RELEASE
   if (gt >= static_cast<uint32_t>(TM::kNA)) named_bar_sync(1 + team, (TM::kTeamWarps + 1) * 32);
+#else
+  if (gt >= static_cast<uint32_t>(TM::kNA)) mbar_wait(s.aempty + 8 * b, ((gt / TM::kNA) - 1) & 1);
+#endif
   PROF_ADD(3);
   if (tw == 0 && lane == 0) TRACE(0, gt);
   HB(4, gt);
@@ -467,10 +499,33 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   HB(7, gt);
 }
 
-template <int NH, class TM>
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
+// Sum of the participating issuers' accumulators (issuer i's columns start
+// i * STRIDE further; fixed ascending order, so the result is deterministic).
+template <int I, uint32_t STRIDE>
+__device__ __forceinline__ void tmem_ld16_sum(uint32_t taddr, uint32_t imask, uint32_t (&r)[16]) {
+  bool first = true;
+#pragma unroll
+  for (int i = 0; i < I; ++i) {
+    if (!((imask >> i) & 1u)) continue;
+    if (first) {
+      tmem_ld16(taddr + i * STRIDE, r);
+      tmem_ld_wait();
+      first = false;
+    } else {
+      uint32_t t[16];
+      tmem_ld16(taddr + i * STRIDE, t);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(t[j]));
+    }
+  }
+}
+
+template <int NH, class TM, int I>
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__((Roles<TM, I>::kMaxRegs))
     spmm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
-  using C = Cfg<NH, TM::kNA>;
+  using C = Cfg<NH, TM::kNA, I>;
+  static_assert(TM::kG == 1, "one afull / aempty barrier per buffer");
   constexpr int NX = C::kNX;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t base = smem_u32(smem_raw);
@@ -485,7 +540,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
   s.aempty = s.afull + 8 * TM::kNP;      // [TM::kNP] both CTAs: MMA commit after the group's last tile
   s.xfull = s.aempty + 8 * TM::kNP;      // [NX] even CTA: 2 arrivals + both halves' bytes
   s.xempty = s.xfull + 8 * NX;       // [NX] both CTAs: MMA commit
-  s.dfull = s.xempty + 8 * NX;       // [2] both CTAs: MMA commit
+  s.dfull = s.xempty + 8 * NX;       // [2] both CTAs: MMA commits of the I issuers
   s.dempty = s.dfull + 16;           // [2] even CTA: 8 arrivals (4 epilogue warps x 2 CTAs)
   s.meta = s.dempty + 16;            // [kMeta] x (stream offset, groups)
   s.tab_s = s.meta + 8 * kMeta;      // [kMaxUnits] unit table: stream offset of the unit
@@ -508,6 +563,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
 
   if (threadIdx.x == 0) {
     TRACE(9, 0);  // kernel start
+#ifdef TCSL_TRACE
+    if (p.trace) p.trace[16 * 4096 + blockIdx.x] = globaltimer_ns();  // every CTA: start (ns)
+#endif
     for (int i = 0; i < kNB; ++i) mbar_init(s.cfull + 8 * i, 1);
     for (int i = 0; i < C::kNR; ++i) mbar_init(s.cempty + 8 * i, 1);
     for (int i = 0; i < TM::kNA; ++i) {
@@ -522,7 +580,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
       mbar_init(s.xempty + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(s.dfull + 8 * i, 1);
+      mbar_init(s.dfull + 8 * i, I);
       mbar_init(s.dempty + 8 * i, 8);
     }
     st_shared_u32(s.tiles_ready, 0u);
@@ -532,7 +590,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
   }
   if (warp == TM::kWarpX && lane == 0) prefetch_tmap(&tmap_x);
   if (warp == TM::kWarpMma) tmem_alloc_pair(s.tmem_slot, C::kTmemCols);
-  for (uint32_t i = threadIdx.x; i < TM::kNA * kABytes / 16; i += TM::kThreads) sts128_zero(s.a + 16 * i);
+  for (uint32_t i = threadIdx.x; i < TM::kNA * kABytes / 16; i += Roles<TM, I>::kThreads) sts128_zero(s.a + 16 * i);
   // Programmatic dependent launch: everything above touches only this CTA's smem,
   // TMEM and parameters, so it overlaps the tail of the previous kernel in the
   // stream; global memory is read and written only after the previous grid has
@@ -595,10 +653,17 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lanes 32q..32q+31 (warp % 4 selects the lane quarter)
     const uint32_t dempty_leader = mapa_shared(s.dempty, 0);
-    uint32_t ui = 0;
+    uint32_t ui = 0, gs0 = 0;  // unit ordinal, X stages of the earlier units
     for (int u = cid; u < p.units; u += ncl, ++ui) {
       const Unit un = unit_of(p, u);
       const uint32_t acc = ui & 1;
+      // issuers that own one of this unit's X stages (stage gs -> issuer gs % I)
+      const uint32_t nst = static_cast<uint32_t>(un.kt1 - un.kt0 + C::kTX - 1) / C::kTX;
+      uint32_t imask = 0;
+#pragma unroll
+      for (int i = 0; i < I; ++i)
+        if (nst >= static_cast<uint32_t>(I) || (static_cast<uint32_t>(i) + I - gs0 % I) % I < nst) imask |= 1u << i;
+      gs0 += nst;
       HB(10, ui);
       // woken by the polling warp once dfull[acc] has completed (a hardware
       // barrier: no issue slots burnt while the unit is computed)
@@ -618,8 +683,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
 #pragma unroll
         for (int c0 = 0; c0 < C::kN; c0 += 16) {
           uint32_t r[16];
-          tmem_ld16(t_base + c0, r);
-          tmem_ld_wait();
+          tmem_ld16_sum<I, 2 * C::kN>(t_base + c0, imask, r);
           if (row_ok && fused) {
             // fused epilogue: act(acc + bias) in fp32, optionally narrowed RNE to binary16
             float v[16];
@@ -787,12 +851,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
     if (ntiles) prefetch_batch();
     bool tab = false;
     long long idle_t0 = clock64();
+    if (!kPollRelease) rel = ntiles;
     while (gt < ntiles || eu < nunits || rel < ntiles) {
       bool progress = false;
       // (d) buffer releases: the MMA of tile rel committed -> wake the team that
       //     decodes tile rel + TM::kNA into the same buffer
       //     (commits come per group of TM::kG buffers: rel is a multiple of TM::kG)
-      while (rel < ntiles &&
+      while (kPollRelease && rel < ntiles &&
              __shfl_sync(0xffffffffu, mbar_test_wait(s.aempty + 8 * ((rel % TM::kNA) / TM::kG), (rel / TM::kNA) & 1) ? 1 : 0, 0)) {
         if (lane == 0) TRACE(15, rel / TM::kG);
         for (uint32_t t = rel; t < rel + TM::kG && t + TM::kNA < ntiles; ++t)
@@ -848,21 +913,20 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
         if (clock64() - idle_t0 > 40000000000LL) __trap();  // watchdog, as in mbar_wait
       }
     }
-  } else if (warp == TM::kWarpMma && rank == 0) {
-    // ---------------------------------------------------------------- MMA issuer (even CTA)
-    // One elected thread runs the whole schedule: no per-tile elect /
-    // reconvergence (-6 % at 90 % sparsity against a warp-wide loop with an
-    // elected issuer, profiles/r01_ablation_mma_loop.txt). Per k-tile: xfull
-    // when an X stage starts, afull once per group of kG tiles, then the 4
-    // MMAs and the commits. Each wait is a ~150-200-cycle sync-unit round
-    // trip even when the phase has completed (profiles/r01_mma_loop_bench.txt).
+  } else if (warp >= TM::kWarpMma && warp < TM::kWarpMma + I && rank == 0) {
+    // ---------------------------------------------------------------- MMA issuers (even CTA)
+    // Issuer ii (one elected thread of warp kWarpMma + ii) owns the X stages
+    // gs = ii (mod I): per stage it waits xfull, then per k-tile the tile's
+    // afull, issues the 4 MMAs into its own accumulator and commits aempty; the
+    // stage's xempty after its last tile. Each mbarrier wait is a ~150-200-cycle
+    // sync-unit round trip even when the phase has completed
+    // (profiles/r01_mma_loop_bench.txt), so one thread waiting per tile caps
+    // the pair near one tile per ~360 cycles; I threads wait in parallel. Every
+    // issuer commits dfull once per unit (dfull counts I arrivals), after the
+    // dempty wait that frees the accumulator pair.
+    const uint32_t ii = static_cast<uint32_t>(warp - TM::kWarpMma);
     const uint64_t a_desc0 = smem_desc(s.a, 128, 1024, 0);
     const uint64_t b_desc0 = smem_desc(s.x, C::kLBO, C::kSBO, C::kLayout);
-    uint32_t total = 0;  // k-tiles of this CTA
-    for (int u = cid; u < p.units; u += ncl) {
-      const Unit un = unit_of(p, u);
-      total += un.kt1 - un.kt0;
-    }
     PROF_DECL(8);  // dempty, xfull, afull, loop, total, fence+descriptors, MMA issue, commits
 #ifdef TCSL_PROFILING
     const long long prof_start = clock64();
@@ -876,60 +940,40 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
         if (ui >= 2) mbar_wait(s.dempty + 8 * acc, ((ui >> 1) - 1) & 1);
         PROF_ADD(0);
         tc_fence_after();
-        const uint32_t d_tmem = tmem + acc * C::kN;
-        int in_stage = 0;
-        for (int kt = un.kt0; kt < un.kt1;) {
+        const uint32_t d_tmem = tmem + ii * (2 * C::kN) + acc * C::kN;
+        uint32_t fresh = 1;  // the first MMA of this issuer in the unit overwrites its accumulator
+        for (int kt = un.kt0; kt < un.kt1; kt += C::kTX, ++gs) {
+          const uint32_t nt = static_cast<uint32_t>(min(C::kTX, un.kt1 - kt));
+          if (I > 1 && gs % I != ii) {
+            gt += nt;
+            continue;
+          }
           const uint32_t xs = gs % NX;
           TRACE(8, gt);
           PROF_ADD(3);
-          if (in_stage == 0) mbar_wait(s.xfull + 8 * xs, (gs / NX) & 1);
+          mbar_wait(s.xfull + 8 * xs, (gs / NX) & 1);
           PROF_ADD(1);
-          const uint32_t b = gt % TM::kNA;
-          // Several k-tiles per iteration when they share an X stage and sit
-          // in consecutive buffers (constant descriptor steps): a whole stage
-          // (kTX = 4 tiles) or a pair; the afull wait of each buffer group
-          // comes right before that group's MMAs.
-          const bool quad = kQuad && C::kTX == 4 && TM::kNA % 4 == 0 && (gt & 3) == 0 && in_stage == 0 &&
-                            kt + 3 < un.kt1;
-          const bool two = !quad && TM::kNA % 2 == 0 && (gt & 1) == 0 && kt + 1 < un.kt1 && in_stage + 1 < C::kTX;
-          const uint32_t nt = quad ? 4u : (two ? 2u : 1u);
-          TRACE(3, gt);
-          if (gt % TM::kG == 0) mbar_wait(s.afull + 8 * (b / TM::kG), (gt / TM::kNA) & 1);  // the group's tiles
-          PROF_ADD(2);
-          TRACE(4, gt);
-          tc_fence_after();
-          const uint64_t ad = a_desc0 + ((b * kABytes) >> 4);
-          const uint64_t bd = b_desc0 + ((xs * C::kXStage + in_stage * C::kTileStep) >> 4);
-          PROF_ADD(5);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (j >= static_cast<int>(nt)) break;
-            if (j > 0 && (gt + j) % TM::kG == 0) {
-              mbar_wait(s.afull + 8 * ((b + j) / TM::kG), (gt / TM::kNA) & 1);
-              tc_fence_after();
-            }
+          const uint64_t bd = b_desc0 + ((xs * C::kXStage) >> 4);
+          for (uint32_t j = 0; j < nt; ++j, ++gt) {
+            const uint32_t b = gt % TM::kNA;
+            TRACE(3, gt);
+            mbar_wait(s.afull + 8 * b, (gt / TM::kNA) & 1);
+            PROF_ADD(2);
+            TRACE(4, gt);
+            tc_fence_after();
+            const uint64_t ad = a_desc0 + ((b * kABytes) >> 4);
+            const uint64_t bdj = bd + ((j * C::kTileStep) >> 4);
 #pragma unroll
             for (int k4 = 0; k4 < kKTB / 16; ++k4)
               if (!DBG(2))
-                mma_f16_ss_pair(d_tmem, ad + ((j * kABytes + k4 * 256) >> 4),
-                                bd + ((j * C::kTileStep + k4 * C::kKStep) >> 4), C::kIdesc,
-                                (kt > un.kt0 || j > 0 || k4 > 0) ? 1u : 0u);
-            if (j + 1 < static_cast<int>(nt) && (gt + j) % TM::kG == TM::kG - 1)
-              mma_commit_pair(s.aempty + 8 * ((b + j) / TM::kG), 3);
+                mma_f16_ss_pair(d_tmem, ad + ((k4 * 256) >> 4), bdj + ((k4 * C::kKStep) >> 4), C::kIdesc,
+                                (fresh && k4 == 0) ? 0u : 1u);
+            fresh = 0;
+            PROF_ADD(6);
+            mma_commit_pair(s.aempty + 8 * b, 3);
+            TRACE(7, gt);
           }
-          PROF_ADD(6);
-          const uint32_t last = gt + nt - 1;
-          if (last % TM::kG == TM::kG - 1 || last + 1 == total) mma_commit_pair(s.aempty + 8 * ((b + nt - 1) / TM::kG), 3);
-          TRACE(7, gt);
-          if (in_stage + static_cast<int>(nt) == C::kTX || kt + static_cast<int>(nt) == un.kt1) {
-            mma_commit_pair(s.xempty + 8 * xs, 3);
-            ++gs;
-            in_stage = 0;
-          } else {
-            in_stage += nt;
-          }
-          kt += nt;
-          gt += nt;
+          mma_commit_pair(s.xempty + 8 * xs, 3);
           PROF_ADD(7);
         }
         mma_commit_pair(s.dfull + 8 * acc, 3);
@@ -939,7 +983,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
 #ifdef TCSL_PROFILING
     PROF_ADD(3);
     prof_.v[4] = clock64() - prof_start;
-    PROF_DUMP(0, 8);
+    if (ii == 0) PROF_DUMP(0, 8);
 #endif
   }
 
@@ -948,6 +992,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(TM::kMaxRegs)
   tc_fence_before();
   cluster_sync_all();
   HB(51, 0);
+#ifdef TCSL_TRACE
+  if (p.trace && threadIdx.x == 0) p.trace[17 * 4096 + blockIdx.x] = globaltimer_ns();  // every CTA: end (ns)
+#endif
   if (warp == TM::kWarpMma) {
     tc_fence_after();
     tmem_dealloc_pair(tmem, C::kTmemCols);
@@ -989,19 +1036,19 @@ int current_device() {
 // Per device (the smem attribute and the occupancy are per-device properties):
 // the >48 KB dynamic-smem opt-in and the co-resident cluster count. Returns 0
 // with *e set when the attribute cannot be applied.
-template <int NH, class TM>
+template <int NH, class TM, int I>
 int max_clusters(cudaError_t* e) {
   static std::atomic<int> cache[kMaxDevices];
   const int dev = current_device();
   int cached = cache[dev].load(std::memory_order_acquire);
   if (!cached) {
-    using C = Cfg<NH, TM::kNA>;
-    *e = cudaFuncSetAttribute(spmm_sm100_kernel<NH, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    using C = Cfg<NH, TM::kNA, I>;
+    *e = cudaFuncSetAttribute(spmm_sm100_kernel<NH, TM, I>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(C::kSmem));
     if (*e != cudaSuccess) return 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * 74, 1, 1);
-    cfg.blockDim = dim3(TM::kThreads, 1, 1);
+    cfg.blockDim = dim3(Roles<TM, I>::kThreads, 1, 1);
     cfg.dynamicSmemBytes = C::kSmem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1011,7 +1058,7 @@ int max_clusters(cudaError_t* e) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nc = 0;
-    if (cudaOccupancyMaxActiveClusters(&nc, spmm_sm100_kernel<NH, TM>, &cfg) != cudaSuccess || nc <= 0) {
+    if (cudaOccupancyMaxActiveClusters(&nc, spmm_sm100_kernel<NH, TM, I>, &cfg) != cudaSuccess || nc <= 0) {
       cudaGetLastError();
       nc = num_sms() / 2;
     }
@@ -1039,18 +1086,18 @@ double split_cost(int tiles_mp, int tiles_k, int split, int clusters, double t_t
   return worst;
 }
 
-template <int NH, class TM>
+template <int NH, class TM, int I>
 cudaError_t launch_shape(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
-  using C = Cfg<NH, TM::kNA>;
+  using C = Cfg<NH, TM::kNA, I>;
   static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
   cudaError_t e = cudaSuccess;
-  const int mc = max_clusters<NH, TM>(&e);
+  const int mc = max_clusters<NH, TM, I>(&e);
   if (e != cudaSuccess) return e;
   const int nc = std::min(clusters, mc);
   if ((p.units + nc - 1) / nc > kMaxUnits) return cudaErrorInvalidConfiguration;  // unit table size
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * nc, 1, 1);
-  cfg.blockDim = dim3(TM::kThreads, 1, 1);
+  cfg.blockDim = dim3(Roles<TM, I>::kThreads, 1, 1);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -1058,7 +1105,7 @@ cudaError_t launch_shape(const Params& p, const CUtensorMap& tm, int clusters, c
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, spmm_sm100_kernel<NH, TM>, tm, p);
+  return cudaLaunchKernelEx(&cfg, spmm_sm100_kernel<NH, TM, I>, tm, p);
 }
 
 // Team shape for a matrix: 2-warp teams while a warp's share of a mean tile
@@ -1073,14 +1120,30 @@ bool dense3_teams(uint64_t n_entries, uint64_t tiles) {
   return mean_groups(n_entries, tiles) <= 0.97 * TeamsDense3::kGK * TeamsDense3::kTeamWarps;
 }
 
+// MMA issuers per team shape (TCSL_ISSUERS overrides, for A/B runs): as many as
+// the TMEM columns allow (2 accumulators of 2 * NH columns each per issuer).
+int issuers_env() {
+  static const int v = getenv("TCSL_ISSUERS") ? atoi(getenv("TCSL_ISSUERS")) : 0;
+  return v;
+}
+template <int NH, class TM>
+cudaError_t launch_iss(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s, int want) {
+  if constexpr (4 * 2 * (2 * NH) <= 512 && Roles<TM, 4>::kThreads <= 1024) {
+    if (want >= 4) return launch_shape<NH, TM, 4>(p, tm, clusters, s);
+  }
+  if constexpr (2 * 2 * (2 * NH) <= 512 && Roles<TM, 2>::kThreads <= 1024) {
+    if (want >= 2) return launch_shape<NH, TM, 2>(p, tm, clusters, s);
+  }
+  return launch_shape<NH, TM, 1>(p, tm, clusters, s);
+}
+
 template <int NH>
 cudaError_t launch_nh(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
   const uint64_t tiles = static_cast<uint64_t>(p.tiles_m) * p.tiles_k;
-  if (sparse_teams(p.n_entries, tiles)) {
-    return launch_shape<NH, TeamsSparse>(p, tm, clusters, s);
-  }
-  if (dense3_teams(p.n_entries, tiles)) return launch_shape<NH, TeamsDense3>(p, tm, clusters, s);
-  return launch_shape<NH, TeamsDense>(p, tm, clusters, s);
+  const int env = issuers_env();
+  if (sparse_teams(p.n_entries, tiles)) return launch_iss<NH, TeamsSparse>(p, tm, clusters, s, env ? env : 2);
+  if (dense3_teams(p.n_entries, tiles)) return launch_iss<NH, TeamsDense3>(p, tm, clusters, s, env ? env : 1);
+  return launch_iss<NH, TeamsDense>(p, tm, clusters, s, env ? env : 1);
 }
 
 }  // namespace
@@ -1203,7 +1266,7 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
 
 }  // namespace tcslk
 
-#ifdef TCSL_PROFILING
+#ifdef TCSL_DEBUG_HOOKS
 extern "C" void tcsl_cuda_debug_set_trace(unsigned long long* d_trace) { tcslk::g_trace = d_trace; }
 #endif
 #if defined(TCSL_TRACE) && defined(TCSL_HEARTBEAT)

@@ -31,7 +31,7 @@ x = tc.gen_synthetic(K, N, 0.0, 2)
 t = tc.encode(w)
 del w
 tc.spmm(t, x, split_k=split)
-trace = torch.zeros(16 * 4096, dtype=torch.int64, device="cuda")
+trace = torch.zeros(18 * 4096, dtype=torch.int64, device="cuda")
 L.tcsl_cuda_debug_set_trace(C.c_void_p(trace.data_ptr()))
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -41,7 +41,15 @@ e.record()
 torch.cuda.synchronize()
 L.tcsl_cuda_debug_set_trace(None)
 print(f"M={M} K={K} N={N} beta={beta} split={split or tc.auto_split(M, K, N)}: {s.elapsed_time(e) * 1e3:.1f} us")
-tr = trace.view(16, 4096).cpu().numpy().astype(np.int64)
+tr = trace.view(18, 4096).cpu().numpy().astype(np.int64)
+nb = int((tr[17] > 0).sum())
+if nb:
+    t0 = tr[16][:nb].min()
+    ends = (tr[17][:nb] - t0) / 1e3
+    starts = (tr[16][:nb] - t0) / 1e3
+    print(f"  CTAs {nb}: start spread {starts.max():.1f} us, end min/median/max {ends.min():.1f} / {np.median(ends):.1f} / {ends.max():.1f} us; slowest CTAs {np.argsort(ends)[-6:].tolist()}")
+if os.environ.get("TRACE_DUMP"):
+    np.save(os.environ["TRACE_DUMP"], tr)
 n = int((tr[4] > 0).sum())
 
 
