@@ -79,6 +79,19 @@ int tcsl_cuda_encode_count(const uint16_t* dW, uint32_t m, uint32_t k, int m_tb,
 int tcsl_cuda_encode_emit(const uint16_t* dW, uint32_t m, uint32_t k, int m_tb, int k_tb, int reorder,
                           const uint32_t* dOffsets, uint32_t* dEntries, int* dErr, void* stream);
 
+/* One pass (W read once): per-tile counts, a decoupled look-back scan for the
+ * offsets, and the entries, in a single kernel. TileConfig {128, 64} with the
+ * bank reorder only (else TCSL_STATUS_UNSUPPORTED); dEntries 16-byte aligned.
+ * dOffsets[0..T] are always written. A tile's entries are written only if
+ * they end within `capacity` entries: when dOffsets[T] exceeds `capacity`,
+ * the caller sizes dEntries from it and runs tcsl_cuda_encode_emit with the
+ * same dOffsets. Same bits as count + emit.
+ * ws: tcsl_cuda_encode_fused_workspace bytes (look-back status words). */
+int tcsl_cuda_encode_fused_workspace(uint32_t m, uint32_t k, int m_tb, int k_tb, size_t* ws_bytes);
+int tcsl_cuda_encode_fused(const uint16_t* dW, uint32_t m, uint32_t k, int m_tb, int k_tb, int reorder,
+                           uint32_t* dOffsets, uint32_t* dEntries, uint64_t capacity, void* ws, size_t ws_bytes,
+                           int* dErr, void* stream);
+
 /* ---------------------------------------------------------------- decode */
 /* Dense m x k binary16 reconstruction (zeros as +0.0). Errors -> *dErr. */
 int tcsl_cuda_decode(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m,

@@ -109,6 +109,8 @@ def lib() -> C.CDLL:
         "tcsl_cuda_encode_workspace": ([u32, u32, i32, i32, C.POINTER(sz)], i32),
         "tcsl_cuda_encode_count": ([vp, u32, u32, i32, i32, vp, vp, sz, vp], i32),
         "tcsl_cuda_encode_emit": ([vp, u32, u32, i32, i32, i32, vp, vp, vp, vp], i32),
+        "tcsl_cuda_encode_fused_workspace": ([u32, u32, i32, i32, C.POINTER(sz)], i32),
+        "tcsl_cuda_encode_fused": ([vp, u32, u32, i32, i32, i32, vp, vp, u64, vp, sz, vp, vp], i32),
         "tcsl_cuda_decode": ([vp, vp, u64, u32, u32, i32, i32, vp, vp, vp], i32),
         "tcsl_cuda_validate": ([vp, u64, u32, u32, i32, i32, vp, vp], i32),
         "tcsl_cuda_spmm_workspace": ([u32, u32, i32, i32, i32, i32, C.POINTER(sz)], i32),
@@ -151,7 +153,7 @@ def lib() -> C.CDLL:
 EXPORTED_SYMBOLS = [
     "tcsl_cuda_abi_version", "tcsl_cuda_status_string", "tcsl_cuda_last_cuda_error", "tcsl_cuda_read_error",
     "tcsl_cuda_encode_workspace", "tcsl_cuda_encode_count", "tcsl_cuda_encode_emit", "tcsl_cuda_decode",
-    "tcsl_cuda_validate", "tcsl_cuda_spmm_workspace", "tcsl_cuda_spmm", "tcsl_cuda_spmm_auto_split",
+    "tcsl_cuda_encode_fused_workspace", "tcsl_cuda_encode_fused", "tcsl_cuda_validate", "tcsl_cuda_spmm_workspace", "tcsl_cuda_spmm", "tcsl_cuda_spmm_auto_split",
     "tcsl_cuda_splitk_reduce", "tcsl_cuda_spmm_exact_workspace", "tcsl_cuda_spmm_exact",
     "tcsl_cuda_rebase_offsets", "tcsl_cuda_gen_synthetic", "tcsl_cuda_malloc", "tcsl_cuda_free",
     "tcsl_cuda_memcpy_h2d", "tcsl_cuda_memcpy_d2h", "tcsl_cuda_memset", "tcsl_cuda_stream_sync",
@@ -261,8 +263,14 @@ def _as_u16(w):
     return w.contiguous()
 
 
-def encode(w, cfg: TileConfig | None = None, reorder: bool = True) -> TcslMatrix:
-    """Dense binary16 W[m, k] (GPU) -> TcslMatrix, bit-exact with tcsl::encode."""
+def encode(w, cfg: TileConfig | None = None, reorder: bool = True, capacity: int | None = None) -> TcslMatrix:
+    """Dense binary16 W[m, k] (GPU) -> TcslMatrix, bit-exact with tcsl::encode.
+
+    Default: two passes (count + scan, then emit into an exactly sized buffer).
+    capacity=C (entries): one pass that reads W once (tcsl_cuda_encode_fused,
+    TileConfig {128, 64} with the reorder) into a C-entry buffer; the result is
+    a view of its first E entries. If E > C the emit pass runs into an exactly
+    sized buffer with the offsets the fused pass computed."""
     torch = _torch()
     cfg = cfg or TileConfig()
     if w.dim() != 2 or w.shape[0] == 0 or w.shape[1] == 0:
@@ -270,15 +278,27 @@ def encode(w, cfg: TileConfig | None = None, reorder: bool = True) -> TcslMatrix
     w = _as_u16(w)
     m, k = w.shape
     L, s = lib(), _stream()
-    ws_bytes = C.c_size_t()
-    _check(L.tcsl_cuda_encode_workspace(m, k, cfg.m_tb, cfg.k_tb, C.byref(ws_bytes)), "encode")
     T = -(-m // cfg.m_tb) * -(-k // cfg.k_tb)
     off = torch.empty(T + 1, dtype=torch.int32, device=w.device)
-    ws = torch.empty(max(ws_bytes.value, 1), dtype=torch.uint8, device=w.device)
-    _check(L.tcsl_cuda_encode_count(_ptr(w), m, k, cfg.m_tb, cfg.k_tb, _ptr(off), _ptr(ws), ws_bytes.value, s))
-    E = int(off[T].item()) & 0xFFFFFFFF
-    ent = torch.empty(E, dtype=torch.int32, device=w.device)
     err = torch.zeros(1, dtype=torch.int32, device=w.device)
+    if capacity is not None and reorder and (cfg.m_tb, cfg.k_tb) == (128, 64):
+        ws_bytes = C.c_size_t()
+        _check(L.tcsl_cuda_encode_fused_workspace(m, k, cfg.m_tb, cfg.k_tb, C.byref(ws_bytes)), "encode")
+        ws = torch.empty(max(ws_bytes.value, 1), dtype=torch.uint8, device=w.device)
+        buf = torch.empty(max(int(capacity), 4), dtype=torch.int32, device=w.device)
+        _check(L.tcsl_cuda_encode_fused(_ptr(w), m, k, cfg.m_tb, cfg.k_tb, 1, _ptr(off), _ptr(buf), int(capacity),
+                                        _ptr(ws), ws_bytes.value, _ptr(err), s), "encode")
+        E = int(off[T].item()) & 0xFFFFFFFF
+        if E <= capacity:
+            _check(L.tcsl_cuda_read_error(_ptr(err), s), "encode")
+            return TcslMatrix(m, k, cfg, reorder, off, buf[:E], tc_ready=True)
+    else:
+        ws_bytes = C.c_size_t()
+        _check(L.tcsl_cuda_encode_workspace(m, k, cfg.m_tb, cfg.k_tb, C.byref(ws_bytes)), "encode")
+        ws = torch.empty(max(ws_bytes.value, 1), dtype=torch.uint8, device=w.device)
+        _check(L.tcsl_cuda_encode_count(_ptr(w), m, k, cfg.m_tb, cfg.k_tb, _ptr(off), _ptr(ws), ws_bytes.value, s))
+        E = int(off[T].item()) & 0xFFFFFFFF
+    ent = torch.empty(E, dtype=torch.int32, device=w.device)
     _check(L.tcsl_cuda_encode_emit(_ptr(w), m, k, cfg.m_tb, cfg.k_tb, int(reorder), _ptr(off), _ptr(ent),
                                    _ptr(err), s))
     _check(L.tcsl_cuda_read_error(_ptr(err), s), "encode")

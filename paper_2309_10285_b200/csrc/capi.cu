@@ -147,6 +147,25 @@ int tcsl_cuda_encode_emit(const uint16_t* dW, uint32_t m, uint32_t k, int m_tb, 
                                                static_cast<cudaStream_t>(stream)));
 }
 
+int tcsl_cuda_encode_fused_workspace(uint32_t m, uint32_t k, int m_tb, int k_tb, size_t* ws_bytes) {
+  if (!tile_ok(m_tb, k_tb) || m == 0 || k == 0 || !ws_bytes) return TCSL_STATUS_INVALID_ARGUMENT;
+  *ws_bytes = tcslk::encode_fused_ws_bytes(num_tiles(m, k, m_tb, k_tb));
+  return TCSL_STATUS_OK;
+}
+
+int tcsl_cuda_encode_fused(const uint16_t* dW, uint32_t m, uint32_t k, int m_tb, int k_tb, int reorder,
+                           uint32_t* dOffsets, uint32_t* dEntries, uint64_t capacity, void* ws, size_t ws_bytes,
+                           int* dErr, void* stream) {
+  if (!tile_ok(m_tb, k_tb) || m == 0 || k == 0 || !dW || !dOffsets || (capacity && !dEntries))
+    return TCSL_STATUS_INVALID_ARGUMENT;
+  if (!tcslk::encode_fused_supported(dW, dEntries, k, m_tb, k_tb, reorder)) return TCSL_STATUS_UNSUPPORTED;
+  size_t need = 0;
+  tcsl_cuda_encode_fused_workspace(m, k, m_tb, k_tb, &need);
+  if (!ws || ws_bytes < need) return TCSL_STATUS_WORKSPACE;
+  return cuda_status(tcslk::launch_encode_fused(dW, m, k, m_tb, k_tb, reorder, dOffsets, dEntries, capacity, ws,
+                                                dErr, static_cast<cudaStream_t>(stream)));
+}
+
 // ------------------------------------------------------------------ decode
 int tcsl_cuda_decode(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m, uint32_t k,
                      int m_tb, int k_tb, uint16_t* dOut, int* dErr, void* stream) {

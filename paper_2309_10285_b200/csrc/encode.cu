@@ -17,6 +17,9 @@
 // Two passes: encode_count_kernel -> exclusive scan (CUB) -> encode_emit_kernel.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "tcsl_internal.cuh"
 
 namespace tcslk {
@@ -40,7 +43,7 @@ __global__ void __launch_bounds__(256) encode_count_kernel(const uint16_t* __res
   const int x_end = static_cast<int>(min(static_cast<long long>(m_tb), static_cast<long long>(m) - r0));
   const int y_end = min(k_tb, static_cast<int>(k) - c0);
   uint32_t cnt = 0;
-  if ((k & 7u) == 0) {
+  if ((k & 7u) == 0 && (reinterpret_cast<uintptr_t>(w) & 15u) == 0) {
     // 16-byte vector loads: rows start 16-B aligned because k % 8 == 0 and c0 % 8 == 0.
     const int vpr = (y_end + 7) >> 3;
     const int total = x_end * vpr;
@@ -372,14 +375,361 @@ __global__ void __launch_bounds__(256) encode_emit_kernel(const uint16_t* __rest
   }
 }
 
+// ============================================================================
+// Fast path for the default TileConfig {128, 64} (every BASELINE shape).
+//
+// Count: one warp per tile (persistent grid), 16-byte loads, a branch-free
+// nonzero test on two binary16 at once: t = v & 0x7FFF7FFF; t + 0x7FFF7FFF has
+// bit 15 (31) set iff the low (high) half is nonzero (no carry crosses halves).
+//
+// Emit (bank reorder): warp w owns the tile rows x = w + 8q (q = 0..15), i.e.
+// exactly the four buckets (w, j) of bank_id(x, y) = (x%8)*4 + (y%8)/2 with
+// j = lane % 4 (lane holds elements y = 2*lane, 2*lane + 1, both in bank column
+// j). The FIFO index of an entry inside its bucket is therefore a running
+// count inside the warp (ballots, no shared memory); only the 32 bucket sizes
+// cross warps (one barrier). Then pos = F(L) + popc(Mask(L) & below(b)) (see
+// the file comment) from a per-tile table of (F, Mask) over L = 1..max c_b, the
+// entries are staged in shared memory and written out with 16-byte stores.
+// ============================================================================
+
+__device__ __forceinline__ uint32_t nz_bits2(uint32_t v) {  // bit 15 / 31 = low / high half nonzero
+  return ((v & 0x7FFF7FFFu) + 0x7FFF7FFFu) & 0x80008000u;
+}
+__device__ __forceinline__ uint32_t ldg_stream(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint4 ldg_nc_v4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_u32_if(uint32_t addr, uint32_t v, uint32_t pred) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}" ::"r"(addr), "r"(v),
+               "r"(pred)
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Requires k % 8 == 0 and a 16-byte aligned W (rows and 8-column chunks are
+// 16-byte aligned; a tile's column fringe is then a whole number of chunks).
+__global__ void __launch_bounds__(256) encode_count128_kernel(const uint16_t* __restrict__ w, uint32_t m, uint32_t k,
+                                                              int tiles_k, uint32_t tiles,
+                                                              uint32_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  const int ch = lane & 7, rr = lane >> 3;  // 8-column chunk, row within a 4-row slab
+  const size_t ld4 = k >> 3;                // row stride in uint4
+  for (uint32_t tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < tiles; tile += nw) {
+    const uint32_t tr = tile / tiles_k, tc = tile - tr * tiles_k;
+    const long long r0 = static_cast<long long>(tr) * 128;
+    const int x_end = static_cast<int>(min(128ll, static_cast<long long>(m) - r0));
+    const bool col_ok = static_cast<uint32_t>(tc * 64 + ch * 8) < k;
+    const uint4* p = reinterpret_cast<const uint4*>(w + r0 * k + tc * 64) + ch + rr * ld4;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      uint4 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int row = 4 * (8 * b + i) + rr;
+        v[i] = (col_ok && row < x_end) ? ldg_nc_v4(p + static_cast<size_t>(4 * (8 * b + i)) * ld4) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t a = nz_bits2(v[i].x) | (nz_bits2(v[i].y) >> 15);
+        const uint32_t c = nz_bits2(v[i].z) | (nz_bits2(v[i].w) >> 15);
+        cnt += __popc(a) + __popc(c);
+      }
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) counts[tile] = (cnt + 31u) & ~31u;
+  }
+}
+
+// Decoupled look-back status word of the fused (one-pass) encoder: bits 32-33
+// = 1 (tile aggregate) or 2 (inclusive prefix), bits 0-31 = the value.
+constexpr unsigned long long kAggregate = 1ull << 32, kPrefix = 2ull << 32;
+
+// FUSED = false: offsets come from the count pass (checked against the tile's
+// own count). FUSED = true: one pass; each tile takes a ticket (tiles in
+// ticket order, so every earlier tile is resident or done), publishes its
+// entry count, finds its base with a warp-wide look-back over earlier tiles'
+// status words, writes offsets[tile + 1], and writes its entries only when
+// they fit in `capacity`.
+//
+// Layout: lane = (rr, ch) holds the 8 elements y = 8ch .. 8ch+7 of row
+// x = w + 8(4q + rr) for slices q = 0..3 (one 16-byte load each). Word j of
+// the load holds both elements of bank column j (y % 8 = 2j, 2j+1), so the
+// four per-column counts of a lane pack into the bytes of one register and a
+// single byte-packed warp scan per slice gives every element's FIFO index
+// (lane order inside a slice is row-major, slices are in row order).
+// One 128 x 64 tile's loads: lane (rr, ch), slice q -> v[q][j] = elements
+// (x, 8ch + 2j), (x, 8ch + 2j + 1) of row x = warp + 8(4q + rr), 0 outside.
+__device__ __forceinline__ void load_tile128(const uint16_t* __restrict__ w, uint32_t m, uint32_t k, int tiles_k,
+                                             uint32_t tile, int warp, int rr, int ch, uint32_t (&v)[4][4]) {
+  const uint32_t tr = tile / tiles_k, tc = tile - tr * tiles_k;
+  const long long r0 = static_cast<long long>(tr) * 128;
+  const int c0 = static_cast<int>(tc) * 64;
+  const int x_end = static_cast<int>(min(128ll, static_cast<long long>(m) - r0));
+  const int y_end = min(64, static_cast<int>(k) - c0);
+  if (x_end == 128 && y_end == 64 && (k & 7u) == 0 && (reinterpret_cast<uintptr_t>(w) & 15u) == 0) {
+    const uint4* p = reinterpret_cast<const uint4*>(w + (r0 + warp + 8 * rr) * k + c0) + ch;
+    const size_t st = static_cast<size_t>(k) * 4;  // 32 rows, in 16-byte units
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 t = ldg_nc_v4(p + q * st);
+      v[q][0] = t.x;
+      v[q][1] = t.y;
+      v[q][2] = t.z;
+      v[q][3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[q][j] = load_raw(w, k, r0, c0, warp + 8 * (4 * q + rr), 8 * ch + 2 * j, x_end, y_end);
+  }
+}
+
+// FUSED = false: offsets come from the count pass (checked against the tile's
+// own count). FUSED = true: one pass; tiles are taken by ticket (so every
+// earlier tile is held by a running block), each publishes its entry count,
+// finds its base with a warp-wide look-back over earlier tiles' status words,
+// writes offsets[tile + 1], and writes its entries only when they fit in
+// `capacity`.
+//
+// One tile per block (persistent blocks that prefetch the next tile measured
+// 17 % slower: fewer resident blocks at the higher register count).
+//
+// Layout: lane = (rr, ch) holds the 8 elements y = 8ch .. 8ch+7 of row
+// x = w + 8(4q + rr) for slices q = 0..3 (one 16-byte load each). Word j of
+// the load holds both elements of bank column j (y % 8 = 2j, 2j+1), so the
+// four per-column counts of a lane pack into the bytes of one register and a
+// single byte-packed warp scan per slice gives every element's FIFO index
+// (lane order inside a slice is row-major, slices are in row order).
+template <bool FUSED>
+__global__ void __launch_bounds__(256, 5) encode_emit128_kernel(const uint16_t* __restrict__ w, uint32_t m,
+                                                                 uint32_t k, int tiles_k, uint32_t tiles,
+                                                                 const uint32_t* __restrict__ offsets_in,
+                                                                 uint32_t* __restrict__ offsets_out,
+                                                                 uint32_t* __restrict__ entries, uint64_t capacity,
+                                                                 unsigned long long* status, uint32_t* ticket,
+                                                                 int* err) {
+  __shared__ uint32_t s_cb[32];
+  __shared__ uint2 s_tab[258];   // (F(L), Mask(L)), L = 1 .. max c_b <= 256
+  __shared__ uint8_t s_zb[1024]; // per (row, 8-column chunk): zero positions (bit = y % 8)
+  __shared__ uint32_t s_misc[4];
+  extern __shared__ __align__(16) uint32_t s_stg[];  // [8192] staged entries
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rr = lane >> 3, ch = lane & 7;
+  const uint32_t stg = static_cast<uint32_t>(__cvta_generic_to_shared(s_stg));
+  uint32_t tile = blockIdx.x;
+  if (FUSED) {
+    if (threadIdx.x == 0) s_misc[0] = atomicAdd(ticket, 1u);
+    __syncthreads();
+    tile = s_misc[0];
+  }
+  uint32_t v[4][4];
+  load_tile128(w, m, k, tiles_k, tile, warp, rr, ch, v);
+  {
+    // ---- FIFO index of each lane's first element per column, packed in bytes
+    uint32_t kidp[4];
+    uint32_t runp = 0;  // per-column counts of the earlier slices (<= 192 each)
+    uint32_t cfin[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t c4 = 0, zm = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t nb = nz_bits2(v[q][j]);
+        c4 |= static_cast<uint32_t>(__popc(nb)) << (8 * j);
+        zm |= (((~nb) >> 15) & 1u) << (2 * j) | (((~nb) >> 31) & 1u) << (2 * j + 1);
+      }
+      uint32_t inc = c4;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
+      }
+      const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+      kidp[q] = runp + inc - c4;
+      if (q < 3) {
+        runp += tot;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cfin[j] = ((runp >> (8 * j)) & 0xFFu) + ((tot >> (8 * j)) & 0xFFu);
+      }
+      s_zb[(warp + 8 * (4 * q + rr)) * 8 + ch] = static_cast<uint8_t>(zm);
+    }
+    if (lane < 4) s_cb[warp * 4 + lane] = lane == 0 ? cfin[0] : (lane == 1 ? cfin[1] : (lane == 2 ? cfin[2] : cfin[3]));
+    __syncthreads();  // (1)
+
+    // ---- (F, Mask) table, tile totals
+    const uint32_t cl = s_cb[lane];
+    const uint32_t nnz = __reduce_add_sync(0xffffffffu, cl);
+    const uint32_t maxc = __reduce_max_sync(0xffffffffu, cl);
+    const uint32_t pad = (32u - (nnz & 31u)) & 31u;
+    const uint32_t total = nnz + pad;
+    for (uint32_t L = warp + 1; L <= maxc; L += 8) {
+      const uint32_t f = __reduce_add_sync(0xffffffffu, cl > L ? cl - L : 0u);
+      const uint32_t mk = __ballot_sync(0xffffffffu, cl >= L);
+      if (lane == 0) s_tab[L] = make_uint2(f, mk);
+    }
+    if (FUSED && warp == 0) {
+      // decoupled look-back
+      if (lane == 0) st_release_gpu_u64(status + tile, (tile == 0 ? kPrefix : kAggregate) | total);
+      uint32_t acc = 0;
+      for (long long jt = static_cast<long long>(tile) - 1; jt >= 0; jt -= 32) {
+        const long long idx = jt - lane;
+        unsigned long long sv = 0;
+        if (idx >= 0) {
+          do {
+            sv = ld_acquire_gpu_u64(status + idx);
+          } while ((sv >> 32) == 0);
+        }
+        const uint32_t pm = __ballot_sync(0xffffffffu, idx >= 0 && (sv >> 32) == 2);
+        const uint32_t val = idx >= 0 ? static_cast<uint32_t>(sv) : 0u;
+        if (pm) {
+          const int f = __ffs(pm) - 1;
+          acc += __reduce_add_sync(0xffffffffu, lane <= f ? val : 0u);
+          break;
+        }
+        acc += __reduce_add_sync(0xffffffffu, val);
+      }
+      if (lane == 0) {
+        if (tile) st_release_gpu_u64(status + tile, kPrefix | (acc + total));
+        offsets_out[tile + 1] = acc + total;
+        if (tile == 0) offsets_out[0] = 0;
+        s_misc[1] = acc;
+      }
+    }
+    uint32_t base = 0;
+    if (!FUSED) {
+      base = offsets_in[tile];
+      if (offsets_in[tile + 1] - base != total) {  // count pass / offsets disagree
+        if (threadIdx.x == 0) raise_dev(err, TCSL_STATUS_INCONSISTENT_OFFSETS);
+        return;
+      }
+    }
+    __syncthreads();  // (2)
+    if (FUSED) base = s_misc[1];
+
+    // ---- +0.0 pads at the first `pad` zero positions, row-major (fringe included)
+    if (pad && warp == 7) {
+      uint32_t zb = 0;
+      for (int x0 = 0; x0 < 128 && zb < pad; x0 += 4) {
+        const uint32_t zm = s_zb[x0 * 8 + lane];  // row x0 + lane / 8, chunk lane % 8: lanes in row-major order
+        const uint32_t n = __popc(zm);
+        uint32_t inc = n;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+          if (lane >= d) inc += t;
+        }
+        uint32_t r = zb + inc - n, mm = zm;
+        const uint32_t loc = static_cast<uint32_t>(x0 + (lane >> 3)) * 64u + 8u * (lane & 7);
+        while (mm && r < pad) {
+          const int bit = __ffs(mm) - 1;
+          mm &= mm - 1;
+          s_stg[nnz + r] = loc + bit;
+          ++r;
+        }
+        zb += __shfl_sync(0xffffffffu, inc, 31);
+      }
+    }
+    // ---- place: pos = F(L) + popc(Mask(L) & below(b)), b = 4 * warp + j;
+    //      branch-free (a zero element's table reads stay in range, 0 <= L <= 256;
+    //      only the stores are predicated)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t xloc = static_cast<uint32_t>(warp + 8 * (4 * q + rr)) * 64u + 8u * ch;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t below = (1u << (warp * 4 + j)) - 1u;
+        const uint32_t r = v[q][j], nb = nz_bits2(r);
+        const uint32_t n0 = (nb >> 15) & 1u;
+        const uint32_t L0 = cfin[j] - ((kidp[q] >> (8 * j)) & 0xFFu);
+        const uint32_t loc0 = xloc + 2u * j;
+        const uint2 t0 = s_tab[L0];
+        const uint2 t1 = s_tab[L0 - n0];
+        sts_u32_if(stg + 4u * (t0.x + __popc(t0.y & below)), __byte_perm(r, loc0, 0x1054), n0);
+        sts_u32_if(stg + 4u * (t1.x + __popc(t1.y & below)), __byte_perm(r, loc0 + 1u, 0x3254), nb >> 31);
+      }
+    }
+    __syncthreads();  // (3)
+    if (!FUSED || static_cast<uint64_t>(base) + total <= capacity) {  // else the host sees offsets[T] > capacity
+      uint4* dst = reinterpret_cast<uint4*>(entries + base);
+      const uint4* src = reinterpret_cast<const uint4*>(s_stg);
+      for (uint32_t i = threadIdx.x; i < total / 4; i += blockDim.x) dst[i] = src[i];
+    }
+  }
+}
+
+constexpr size_t kEmit128Dyn = 8192 * 4;
+
+bool fast128(const void* w, uint32_t k, int m_tb, int k_tb) {
+  return m_tb == 128 && k_tb == 64 && (k & 7u) == 0 && (reinterpret_cast<uintptr_t>(w) & 15u) == 0;
+}
+
 }  // namespace
 
 cudaError_t launch_encode_count(const uint16_t* w, uint32_t m, uint32_t k, int m_tb, int k_tb,
                                 uint32_t* counts, cudaStream_t s) {
   const int tk = div_up_i(k, k_tb);
   const long long tiles = static_cast<long long>(div_up_i(m, m_tb)) * tk;
-  if (tiles > 0) encode_count_kernel<<<static_cast<unsigned>(tiles), 256, 0, s>>>(w, m, k, m_tb, k_tb, tk, counts);
+  if (tiles <= 0) return cudaSuccess;
+  if (fast128(w, k, m_tb, k_tb) && !getenv("TCSL_ENCODE_SLOW")) {
+    const long long blocks = std::min<long long>((tiles + 7) / 8, 148ll * 16);
+    encode_count128_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(w, m, k, tk, static_cast<uint32_t>(tiles),
+                                                                        counts);
+    return cudaGetLastError();
+  }
+  encode_count_kernel<<<static_cast<unsigned>(tiles), 256, 0, s>>>(w, m, k, m_tb, k_tb, tk, counts);
   return cudaGetLastError();
+}
+
+size_t encode_fused_ws_bytes(uint32_t tiles) { return 256 + 8ull * tiles; }
+
+cudaError_t launch_encode_fused(const uint16_t* w, uint32_t m, uint32_t k, int m_tb, int k_tb, int reorder,
+                                uint32_t* offsets, uint32_t* entries, uint64_t capacity, void* ws, int* err,
+                                cudaStream_t s) {
+  (void)m_tb;
+  (void)k_tb;
+  (void)reorder;
+  const int tk = div_up_i(k, 64);
+  const long long tiles = static_cast<long long>(div_up_i(m, 128)) * tk;
+  cudaError_t e = cudaMemsetAsync(ws, 0, encode_fused_ws_bytes(static_cast<uint32_t>(tiles)), s);
+  if (e != cudaSuccess || tiles <= 0) return e;
+  auto* ticket = static_cast<uint32_t*>(ws);
+  auto* status = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256);
+  e = cudaFuncSetAttribute(encode_emit128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(kEmit128Dyn));
+  if (e != cudaSuccess) return e;
+  encode_emit128_kernel<true><<<static_cast<unsigned>(tiles), 256, kEmit128Dyn, s>>>(w, m, k, tk, static_cast<uint32_t>(tiles), nullptr, offsets, entries,
+                                                                            capacity, status, ticket, err);
+  return cudaGetLastError();
+}
+
+bool encode_fused_supported(const void* w, const void* entries, uint32_t k, int m_tb, int k_tb, int reorder) {
+  (void)w;
+  (void)k;
+  return reorder && m_tb == 128 && k_tb == 64 && (reinterpret_cast<uintptr_t>(entries) & 15u) == 0;
 }
 
 size_t encode_scan_temp_bytes(uint32_t tiles) {
@@ -398,6 +748,15 @@ cudaError_t launch_encode_emit(const uint16_t* w, uint32_t m, uint32_t k, int m_
                                const uint32_t* offsets, uint32_t* entries, int* err, cudaStream_t s) {
   const int tk = div_up_i(k, k_tb);
   const long long tiles = static_cast<long long>(div_up_i(m, m_tb)) * tk;
+  if (tiles > 0 && reorder && m_tb == 128 && k_tb == 64 && (reinterpret_cast<uintptr_t>(entries) & 15u) == 0 &&
+      !getenv("TCSL_ENCODE_SLOW")) {
+    cudaError_t e = cudaFuncSetAttribute(encode_emit128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kEmit128Dyn));
+    if (e != cudaSuccess) return e;
+    encode_emit128_kernel<false><<<static_cast<unsigned>(tiles), 256, kEmit128Dyn, s>>>(w, m, k, tk, static_cast<uint32_t>(tiles), offsets, nullptr, entries,
+                                                                               0, nullptr, nullptr, err);
+    return cudaGetLastError();
+  }
   const EmitLayout lay = emit_layout(m_tb, k_tb);
   cudaError_t e = cudaFuncSetAttribute(encode_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(lay.bytes));

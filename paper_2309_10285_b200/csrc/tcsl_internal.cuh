@@ -74,6 +74,12 @@ cudaError_t launch_validate_entries(const uint32_t* off, const uint32_t* ent, ui
                                     uint32_t k, int m_tb, int k_tb, int strict, uint32_t* flags, int* err,
                                     cudaStream_t s);
 size_t encode_scan_temp_bytes(uint32_t tiles);
+// One-pass encoder (count + emit with a decoupled look-back; TileConfig {128, 64}, reorder).
+size_t encode_fused_ws_bytes(uint32_t tiles);
+bool encode_fused_supported(const void* w, const void* entries, uint32_t k, int m_tb, int k_tb, int reorder);
+cudaError_t launch_encode_fused(const uint16_t* w, uint32_t m, uint32_t k, int m_tb, int k_tb, int reorder,
+                                uint32_t* offsets, uint32_t* entries, uint64_t capacity, void* ws, int* err,
+                                cudaStream_t s);
 cudaError_t launch_encode_scan(uint32_t* counts_in, uint32_t* offsets, uint32_t tiles, void* temp,
                                size_t temp_bytes, cudaStream_t s);
 cudaError_t launch_validate(const uint32_t* off, uint64_t n_entries, uint32_t tiles, int* err,

@@ -153,3 +153,72 @@ def test_shard_slices_equal_reencoding(port):
             off, ent = sh.to_host()
             want = port.encode(a[tr0 * 128:min(1000, tr1 * 128)])
             assert (off == want.offsets).all() and (ent == want.entries).all()
+
+
+def _fused_same(a, slack=0):
+    """The one-pass encoder (tcsl_cuda_encode_fused) gives count+emit's bits."""
+    import paper_2309_10285_b200 as tc
+    w = _dev(a)
+    t = tc.encode(w)
+    tf = tc.encode(w, capacity=t.n_entries + slack)
+    off, ent = t.to_host()
+    offf, entf = tf.to_host()
+    assert (off == offf).all() and (ent == entf).all()
+    return t
+
+
+def test_fused_encoder_matches_two_pass(port):
+    rng = np.random.default_rng(77)
+    for it in range(10):
+        m, k = int(rng.integers(1, 900)), int(rng.integers(1, 900))
+        beta = float(rng.choice([0.0, 0.5, 0.8, 0.9, 0.99, 1.0]))
+        a = port.gen_random_sparse(m, k, beta, int(rng.integers(0, 2**62)))
+        t = _fused_same(a, slack=int(rng.integers(0, 100)))
+        want = port.encode(a)
+        off, ent = t.to_host()
+        assert (off == want.offsets).all() and (ent == want.entries).all()
+
+
+def test_fused_encoder_full_size_and_overflow(port):
+    """OPT-66B FFN1 at 80 %: one pass == two passes; a too-small capacity falls back
+    to emit with the fused pass's offsets."""
+    import torch
+
+    import paper_2309_10285_b200 as tc
+    w = tc.gen_synthetic(36864, 9216, 0.8, 3)
+    t = tc.encode(w)
+    tf = tc.encode(w, capacity=t.n_entries)
+    assert torch.equal(t.offsets, tf.offsets) and torch.equal(t.entries, tf.entries)
+    small = tc.encode(w, capacity=t.n_entries // 2)
+    assert torch.equal(t.offsets, small.offsets) and torch.equal(t.entries, small.entries)
+
+
+def test_encoder_unaligned_and_odd_widths(port):
+    """Fast-path guards: a W view that is not 16-byte aligned, odd k, k % 8 != 0."""
+    import paper_2309_10285_b200 as tc
+    a = port.gen_random_sparse(300, 513, 0.7, 9)
+    big = _dev(a.reshape(-1))
+    for (m, k, shift) in [(300, 512, 1), (299, 511, 3), (257, 136, 0), (130, 66, 2)]:
+        w = big[shift:shift + m * k].view(m, k)
+        t = tc.encode(w)
+        want = port.encode(w.cpu().numpy().view(np.uint16))
+        off, ent = t.to_host()
+        assert (off == want.offsets).all() and (ent == want.entries).all(), (m, k, shift)
+        _fused_same(w.cpu().numpy().view(np.uint16))
+
+
+def test_encoder_extreme_bank_counts(port):
+    """Every element nonzero (c_b = 256 for all banks), one bank column only, one row only."""
+    rng = np.random.default_rng(3)
+    full = rng.integers(1, 0x7BFF, size=(256, 128), dtype=np.uint32).astype(np.uint16)
+    _same(port, full)
+    col = np.zeros((128, 64), np.uint16)
+    col[:, 0::8] = 0x3C00
+    _same(port, col)
+    row = np.zeros((128, 64), np.uint16)
+    row[5, :] = 0x3C00
+    row[5, 7] = 0x8000  # -0.0: numerically zero, becomes a pad position candidate
+    _same(port, row)
+    _fused_same(full)
+    _fused_same(col)
+    _fused_same(row)
