@@ -735,36 +735,44 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__((Roles<TM, I>::kMaxRegs))
     // unit boundaries); chunk k lands on cfull[k % kNB], decoders count consumed
     // bytes on cempty[k % C::kNR] (complete_tx). A bulk-copy issue blocks for
     // hundreds of cycles under load, so this warp does nothing else.
-    // 1. Validate every unit (monotone offsets, whole 32-entry groups, in range)
-    //    into the unit table; an invalid unit streams no bytes and its tiles
-    //    decode as empty (the error is reported).
-    uint32_t total = 0, nunits = 0;
-    for (int u = cid; u < p.units; u += ncl, ++nunits) {
-      const Unit un = unit_of(p, u);
-      const int rb = 2 * un.rp + static_cast<int>(rank);
-      const uint32_t nt = un.kt1 - un.kt0;
+    // 1. Unit table: the unit's entry span [g0, g1) = [offsets[first tile],
+    //    offsets[last tile + 1]), one lane per unit (all loads in one round trip).
+    //    A span that is not in range or not whole groups streams nothing (its
+    //    tiles decode as empty, inconsistent_offsets is raised). Per-tile
+    //    offsets are checked by the polling warp as it publishes the tiles'
+    //    metadata (it clamps them into the span, so the streamed bytes are
+    //    always consumed exactly).
+    uint32_t total = 0;
+    for (uint32_t u0 = 0;; u0 += 32) {
+      const int u = cid + static_cast<int>(u0 + lane) * ncl;
       uint32_t g0 = 0, g1 = 0;
-      if (rb < p.tiles_m) {
-        const uint32_t t0 = static_cast<uint32_t>(rb) * p.tiles_k + un.kt0;
-        g0 = __ldg(p.off + t0);
-        g1 = __ldg(p.off + t0 + nt);
-        bool bad = g0 > g1 || g1 > p.n_entries || (g0 & 31u) != 0;
-#pragma unroll 16
-        for (uint32_t i = lane; i < nt; i += 32) {
-          const uint32_t a = __ldg(p.off + t0 + i), b = __ldg(p.off + t0 + i + 1);
-          bad |= b < a || ((b - a) & 31u) != 0;
-        }
-        if (__any_sync(0xffffffffu, bad)) {
-          if (lane == 0) raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
-          g1 = g0;
+      if (u < p.units) {
+        const Unit un = unit_of(p, u);
+        const int rb = 2 * un.rp + static_cast<int>(rank);
+        if (rb < p.tiles_m) {
+          const uint32_t t0 = static_cast<uint32_t>(rb) * p.tiles_k + un.kt0;
+          g0 = __ldg(p.off + t0);
+          g1 = __ldg(p.off + t0 + (un.kt1 - un.kt0));
+          if (g0 > g1 || g1 > p.n_entries || ((g0 | g1) & 31u) != 0) {
+            raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
+            g1 = g0;
+          }
         }
       }
-      if (lane == 0) {
-        st_shared_u32(s.tab_s + 4 * nunits, total);
-        st_shared_u32(s.tab_g0 + 4 * nunits, g0);
-        st_shared_u32(s.tab_g1 + 4 * nunits, g1);
+      const uint32_t bytes = (g1 - g0) * 4u;
+      uint32_t inc = bytes;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
       }
-      total += (g1 - g0) * 4u;
+      if (u < p.units) {
+        st_shared_u32(s.tab_s + 4 * (u0 + lane), total + inc - bytes);
+        st_shared_u32(s.tab_g0 + 4 * (u0 + lane), g0);
+        st_shared_u32(s.tab_g1 + 4 * (u0 + lane), g1);
+      }
+      total += __shfl_sync(0xffffffffu, inc, 31);
+      if (cid + static_cast<int>(u0 + 32) * ncl >= p.units) break;
     }
     __syncwarp();
     if (lane == 0) {
@@ -834,17 +842,17 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__((Roles<TM, I>::kMaxRegs))
     }
     uint32_t gt = 0, mu = 0, mkt = 0;  // (a) next tile to publish: unit ordinal, k-tile within the unit
     int mu_id = cid;
-    uint32_t pend = 0, pa0 = 0, pa1 = 0;  //     prefetched batch: tile count, this lane's offsets
+    uint32_t pend = 0, pa1 = 0;        //     prefetched batch: tile count, this lane's offsets[tile + 1]
+    uint32_t mcarry = 0;               //     end of the last published tile's (clamped) span
     uint32_t eu = 0;                   // (c) next unit whose accumulator the epilogue waits for
     uint32_t rel = 0;                  // (d) next tile whose MMA completion releases its buffer
     auto prefetch_batch = [&]() {
       const Unit un = unit_of(p, mu_id);
       const int rb = 2 * un.rp + static_cast<int>(rank);
       pend = min(32u, static_cast<uint32_t>(un.kt1 - un.kt0) - mkt);
-      pa0 = pa1 = 0;
+      pa1 = 0;
       if (rb < p.tiles_m && lane < pend) {
         const uint32_t t = static_cast<uint32_t>(rb) * p.tiles_k + un.kt0 + mkt + lane;
-        pa0 = __ldg(p.off + t);
         pa1 = __ldg(p.off + t + 1);
       }
     };
@@ -877,14 +885,30 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__((Roles<TM, I>::kMaxRegs))
       if (pend && tab) {
         const uint32_t room = __shfl_sync(0xffffffffu, ld_acquire_u32(s.done), 0) + (kMeta - 16);
         if (gt + pend <= room) {
-          if (lane < pend) {
+          {
+            // tile lane's span [b, e): its offsets clamped into the unit's span
+            // [g0, g1) and made monotone (running max), whole groups; any
+            // correction raises inconsistent_offsets (check_offsets,
+            // tcsl_format.cpp:19-32). The unit's streamed bytes are then
+            // consumed exactly whatever the offsets hold.
             const uint32_t g0 = lds32(s.tab_g0 + 4 * mu), g1 = lds32(s.tab_g1 + 4 * mu);
-            uint32_t so = lds32(s.tab_s + 4 * mu), ng = 0;
-            if (g1 > g0) {  // real rows of a valid, non-empty unit
-              so += (pa0 - g0) * 4u;
-              ng = (pa1 - pa0) >> 5;
+            if (mkt == 0) mcarry = g0;  // first tile of the unit starts at g0 (= its offsets[first tile])
+            uint32_t e = lane < pend ? g0 + ((min(max(pa1, g0), g1) - g0) & ~31u) : 0u;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) e = max(e, __shfl_up_sync(0xffffffffu, e, d));
+            e = max(e, mcarry);
+            uint32_t b = __shfl_up_sync(0xffffffffu, e, 1);
+            if (lane == 0) b = mcarry;
+            if (lane < pend) {
+              if (g1 > g0 && (e != pa1 || b > e)) raise_dev(p.err, TCSL_STATUS_INCONSISTENT_OFFSETS);
+              uint32_t so = lds32(s.tab_s + 4 * mu), ng = 0;
+              if (g1 > g0) {  // real rows of a valid, non-empty unit
+                so += (b - g0) * 4u;
+                ng = (e - b) >> 5;
+              }
+              st_shared_v2(s.meta + 8 * ((gt + lane) % kMeta), so, ng);
             }
-            st_shared_v2(s.meta + 8 * ((gt + lane) % kMeta), so, ng);
+            mcarry = __shfl_sync(0xffffffffu, e, pend - 1);
           }
           __threadfence_block();
           __syncwarp();
