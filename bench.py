@@ -449,7 +449,7 @@ def run_ours(args, rank, world):
     by_beta = {}
     for b in BETAS:
         rows = [r for r in cell_rows if r["sparsity"] == b]
-        if rows:
+        if rows and sum(r["us"] for r in rows) > 0:  # (per-cell times are ~0 under a serialising profiler)
             by_beta[str(b)] = round(sum(r["gbs"] * r["us"] for r in rows) / sum(r["us"] for r in rows) / hbm_peak, 3)
     result["roofline"] = {
         "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",

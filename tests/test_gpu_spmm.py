@@ -161,6 +161,36 @@ def test_errors(port):
         tc.spmm(t, _dev(port.gen_random_sparse(128, 8, 0.0, 2)), out=torch.empty((256, 4), device="cuda"))
 
 
+@pytest.mark.timeout(300)
+def test_corrupt_tile_offsets_kernel_path(port):
+    """The tensor-core kernel itself (tc_ready forced, so no host/device pre-check routes the
+    matrix elsewhere) on per-tile offsets corrupted inside a work unit: non-monotone,
+    not whole groups, past the unit's span. Each raises inconsistent_offsets and returns
+    (the polling warp clamps the spans, so the streamed bytes are consumed exactly); an
+    intact matrix afterwards still computes correctly."""
+    import paper_2309_10285_b200 as tc
+    a = port.gen_random_sparse(1024, 2048, 0.8, 5)
+    x = port.gen_random_sparse(2048, 16, 0.0, 6)
+    t = tc.encode(_dev(a))
+    tk = t.tiles_k if hasattr(t, "tiles_k") else -(-t.k // 64)
+    mid = 3 * tk + 11  # a tile inside row block 3's unit
+    for kind in ("down", "partial", "past"):
+        off = t.offsets.clone()
+        if kind == "down":
+            off[mid] = off[mid - 1] - 32 if int(off[mid - 1]) >= 32 else 0
+        elif kind == "partial":
+            off[mid] += 16
+        else:
+            off[mid] = off[mid + 5] + 64
+        bad = tc.TcslMatrix(t.m, t.k, t.cfg, True, off, t.entries, tc_ready=True)
+        for split in (1, 3):
+            with pytest.raises(tc.TcslError, match="inconsistent_offsets"):
+                tc.spmm(bad, _dev(x), split_k=split)
+    want = port.spmm(port.encode(a), x, 4)
+    y = tc.spmm(t, _dev(x)).cpu().numpy()
+    assert np.linalg.norm(y - want) / np.linalg.norm(want) <= 1e-3
+
+
 def test_sharded_rows_match_full(port):
     """Row shards (multi-GPU layout) reproduce the full result bit for bit with split_k=1."""
     import torch
