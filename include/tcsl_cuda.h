@@ -171,6 +171,18 @@ int tcsl_cuda_spmm_ex(const uint32_t* dOffsets, const uint32_t* dEntries, uint64
                       const float* dBias, int activation, int split_k, int exact, void* ws, size_t ws_bytes,
                       int* dErr, void* stream);
 /* The split the automatic heuristic picks for this shape on this device. */
+/* Row-sharded SpMM with the all-gather fused into the epilogue (SURVEY.md §8e,
+ * configs[4]): as tcsl_cuda_spmm_ex, but every finished Y row block is stored
+ * into each of the n_peers (<= TCSL_MAX_PEERS) destinations dPeerY[g] (a DEVICE
+ * array of device pointers: rank g's full-Y buffer, already offset to this
+ * shard's first row; peer pointers are NVLink-mapped, e.g. symmetric memory), so
+ * no collective runs after the kernel; the caller's cross-rank barrier makes the
+ * rows visible. With split-K the epilogue pass (K3) does the pushing. */
+#define TCSL_MAX_PEERS 64
+int tcsl_cuda_spmm_push(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m,
+                        uint32_t k, int m_tb, int k_tb, const uint16_t* dX, int n, void* const* dPeerY, int n_peers,
+                        int out_dtype, const float* dBias, int activation, int split_k, int exact, void* ws,
+                        size_t ws_bytes, int* dErr, void* stream);
 int tcsl_cuda_spmm_auto_split(uint32_t m, uint32_t k, int n);
 /* Y = sum_{s=0}^{S-1} P[s] in ascending s (P is S x count floats). */
 int tcsl_cuda_splitk_reduce(const float* dPartials, int split_k, size_t count, float* dY, void* stream);

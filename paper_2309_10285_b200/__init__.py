@@ -134,6 +134,8 @@ def lib() -> C.CDLL:
         "tcsl_cuda_spmm_ex_workspace": ([u32, u32, i32, i32, i32, i32, i32, C.POINTER(sz)], i32),
         "tcsl_cuda_spmm_ex": ([vp, vp, u64, u32, u32, i32, i32, vp, i32, vp, i32, vp, i32, i32, i32, vp, sz, vp,
                                vp], i32),
+        "tcsl_cuda_spmm_push": ([vp, vp, u64, u32, u32, i32, i32, vp, i32, vp, i32, i32, vp, i32, i32, i32, vp, sz,
+                                 vp, vp], i32),
         "tcsl_cuda_prune_workspace": ([u64, C.POINTER(sz)], i32),
         "tcsl_cuda_prune_magnitude": ([vp, u64, C.c_double, vp, vp, sz, vp], i32),
         "tcsl_cuda_nccl_available": ([], i32),
@@ -158,7 +160,7 @@ EXPORTED_SYMBOLS = [
     "tcsl_cuda_rebase_offsets", "tcsl_cuda_gen_synthetic", "tcsl_cuda_malloc", "tcsl_cuda_free",
     "tcsl_cuda_memcpy_h2d", "tcsl_cuda_memcpy_d2h", "tcsl_cuda_memset", "tcsl_cuda_stream_sync",
     "tcsl_cuda_device_count", "tcsl_cuda_validate_entries", "tcsl_cuda_parse_header", "tcsl_cuda_ingest",
-    "tcsl_cuda_spmm_ex_workspace", "tcsl_cuda_spmm_ex", "tcsl_cuda_prune_workspace", "tcsl_cuda_prune_magnitude",
+    "tcsl_cuda_spmm_ex_workspace", "tcsl_cuda_spmm_ex", "tcsl_cuda_spmm_push", "tcsl_cuda_prune_workspace", "tcsl_cuda_prune_magnitude",
     "tcsl_cuda_nccl_available", "tcsl_cuda_nccl_unique_id", "tcsl_cuda_nccl_comm_init",
     "tcsl_cuda_nccl_comm_destroy", "tcsl_cuda_allgather_rows",
 ]
@@ -424,6 +426,47 @@ def spmm(t: TcslMatrix, x, split_k: int = 0, exact: bool = False, out=None, ws: 
     if check:
         _check(L.tcsl_cuda_read_error(_ptr(err), s), "spmm")
     return out
+
+
+def spmm_push(t: TcslMatrix, x, peer_ptrs, split_k: int = 0, exact: bool = False, ws: SpmmWorkspace | None = None,
+              check: bool = True, bias=None, activation: str | None = None, out_dtype=None) -> None:
+    """Row-shard SpMM with the all-gather fused into the epilogue (tcsl_cuda_spmm_push):
+    Y = activation(t @ X + bias) is stored into every destination of `peer_ptrs` (an int64
+    device tensor of device addresses — each rank's full-Y buffer offset to this shard's
+    first row, e.g. symmetric-memory peer buffers) instead of a local output. The
+    caller's cross-rank barrier then makes the rows visible (sharding.RowShardedSpmm)."""
+    torch = _torch()
+    if x.dim() != 2 or x.shape[0] != t.k or x.shape[1] == 0:
+        raise TcslError(9, f"A has {t.k} columns, B has {x.shape[0] if x.dim() == 2 else '?'} rows")
+    x = _as_u16(x)
+    n = x.shape[1]
+    dev = t.offsets.device
+    if x.device != dev or peer_ptrs.device != dev or peer_ptrs.dtype != torch.int64 or peer_ptrs.dim() != 1:
+        raise TcslError(10, "X and peer_ptrs (int64 addresses) must be on the matrix's device")
+    if t.offsets.numel() != t.num_tiles + 1:
+        raise TcslError(7, "offset table must have num_tiles+1 entries")
+    if activation not in ACTIVATIONS:
+        raise TcslError(10, f"unknown activation {activation!r}")
+    out_dtype = out_dtype or torch.float32
+    if out_dtype not in (torch.float32, torch.float16):
+        raise TcslError(10, f"output dtype must be float32 or float16, got {out_dtype}")
+    if bias is not None and (bias.dtype != torch.float32 or bias.numel() != t.m or bias.device != dev):
+        raise TcslError(10, f"bias must be a float32 tensor of {t.m} elements on {dev}")
+    if not exact and t.cfg.m_tb == 128 and t.cfg.k_tb == 64 and not _tc_ready(t):
+        exact = True
+    L, s = lib(), _stream()
+    ws = ws or _default_ws
+    nb = C.c_size_t()
+    _check(L.tcsl_cuda_spmm_ex_workspace(t.m, t.k, t.cfg.m_tb, t.cfg.k_tb, n, split_k, int(exact), C.byref(nb)))
+    buf, err = ws.get(nb.value, dev)
+    if check:
+        err.zero_()
+    _check(L.tcsl_cuda_spmm_push(_ptr(t.offsets), _ptr(t.entries), t.n_entries, t.m, t.k, t.cfg.m_tb, t.cfg.k_tb,
+                                 _ptr(x), n, _ptr(peer_ptrs), peer_ptrs.numel(), int(out_dtype == torch.float16),
+                                 _ptr(bias), ACTIVATIONS[activation], split_k, int(exact), _ptr(buf), buf.numel(),
+                                 _ptr(err), s), "spmm")
+    if check:
+        _check(L.tcsl_cuda_read_error(_ptr(err), s), "spmm")
 
 
 def auto_split(m: int, k: int, n: int) -> int:

@@ -363,17 +363,23 @@ int tcsl_cuda_spmm(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t 
                            TCSL_ACT_NONE, split_k, 0, ws, ws_bytes, dErr, stream);
 }
 
-int tcsl_cuda_spmm_ex(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m,
-                      uint32_t k, int m_tb, int k_tb, const uint16_t* dX, int n, void* dY, int out_dtype,
-                      const float* dBias, int activation, int split_k, int exact, void* ws, size_t ws_bytes,
-                      int* dErr, void* stream) {
+namespace {
+
+// tcsl_cuda_spmm_ex and tcsl_cuda_spmm_push: Y to dY, or (n_peers > 0) to every
+// dPeers[g] (device array of base pointers) through the epilogue pass.
+int spmm_core(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m, uint32_t k,
+              int m_tb, int k_tb, const uint16_t* dX, int n, void* dY, int out_dtype, void* const* dPeers,
+              int n_peers, const float* dBias, int activation, int split_k, int exact, void* ws, size_t ws_bytes,
+              int* dErr, void* stream) {
   // engine.cpp:28-32 (the dimension check is the caller's: no B shape crosses the ABI)
   if (!tile_ok(m_tb, k_tb) || n <= 0 || m == 0 || k == 0 || split_k < 0) return TCSL_STATUS_INVALID_ARGUMENT;
   if (out_dtype != TCSL_OUT_F32 && out_dtype != TCSL_OUT_F16) return TCSL_STATUS_INVALID_ARGUMENT;
   if (activation < TCSL_ACT_NONE || activation > TCSL_ACT_GELU_TANH) return TCSL_STATUS_INVALID_ARGUMENT;
-  if (!dOffsets || !dX || !dY || (n_entries && !dEntries)) return TCSL_STATUS_INVALID_ARGUMENT;
+  if (!dOffsets || !dX || (n_peers > 0 ? !dPeers : !dY) || n_peers < 0 || (n_entries && !dEntries))
+    return TCSL_STATUS_INVALID_ARGUMENT;
   auto s = static_cast<cudaStream_t>(stream);
-  const bool fused = dBias != nullptr || activation != TCSL_ACT_NONE || out_dtype == TCSL_OUT_F16;
+  const bool push = n_peers > 0;
+  const bool fused = dBias != nullptr || activation != TCSL_ACT_NONE || out_dtype == TCSL_OUT_F16 || push;
   float* y32 = out_dtype == TCSL_OUT_F32 ? static_cast<float*>(dY) : nullptr;
   uint16_t* y16 = out_dtype == TCSL_OUT_F16 ? static_cast<uint16_t*>(dY) : nullptr;
   cudaError_t e = cudaSuccess;
@@ -384,7 +390,9 @@ int tcsl_cuda_spmm_ex(const uint32_t* dOffsets, const uint32_t* dEntries, uint64
     float* tmp = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(static_cast<size_t>(m) * k * 2));
     e = tcslk::launch_decode(dOffsets, dEntries, n_entries, m, k, m_tb, k_tb, dense, dErr, 0, s);
     if (e == cudaSuccess) e = tcslk::launch_dense_gemm_exact(dense, m, k, dX, n, fused ? tmp : y32, s);
-    if (e == cudaSuccess && fused) e = tcslk::launch_reduce_epilogue(tmp, 1, m, n, dBias, activation, y32, y16, s);
+    if (e == cudaSuccess && fused)
+      e = tcslk::launch_reduce_epilogue(tmp, 1, m, n, dBias, activation, y32, y16, s, dPeers, n_peers,
+                                        out_dtype == TCSL_OUT_F16);
     return cuda_status(e);
   }
   // cp.async.bulk streams 128-B spans of the entries: they must be 16-B aligned
@@ -411,16 +419,40 @@ int tcsl_cuda_spmm_ex(const uint32_t* dOffsets, const uint32_t* dEntries, uint64
     float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + lay.x_pad);
     e = tcslk::launch_spmm_sm100(plan, dOffsets, dEntries, n_entries, m, k, x, ldx, part, dErr, s);
     if (e == cudaSuccess)
-      e = fused ? tcslk::launch_reduce_epilogue(part, split, m, n, dBias, activation, y32, y16, s)
+      e = fused ? tcslk::launch_reduce_epilogue(part, split, m, n, dBias, activation, y32, y16, s, dPeers, n_peers,
+                                                out_dtype == TCSL_OUT_F16)
                 : tcslk::launch_splitk_reduce(part, split, static_cast<size_t>(m) * n, y32, s);
   } else {
     tcslk::Epilogue epi;
     epi.bias = dBias;
     epi.act = activation;
     epi.out16 = y16;
+    epi.peers = dPeers;
+    epi.n_peers = n_peers;
+    epi.peers_f16 = out_dtype == TCSL_OUT_F16;
     e = tcslk::launch_spmm_sm100(plan, dOffsets, dEntries, n_entries, m, k, x, ldx, y32, dErr, s, epi);
   }
   return cuda_status(e);
+}
+
+}  // namespace
+
+int tcsl_cuda_spmm_ex(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m,
+                      uint32_t k, int m_tb, int k_tb, const uint16_t* dX, int n, void* dY, int out_dtype,
+                      const float* dBias, int activation, int split_k, int exact, void* ws, size_t ws_bytes,
+                      int* dErr, void* stream) {
+  if (!dY) return TCSL_STATUS_INVALID_ARGUMENT;
+  return spmm_core(dOffsets, dEntries, n_entries, m, k, m_tb, k_tb, dX, n, dY, out_dtype, nullptr, 0, dBias,
+                   activation, split_k, exact, ws, ws_bytes, dErr, stream);
+}
+
+int tcsl_cuda_spmm_push(const uint32_t* dOffsets, const uint32_t* dEntries, uint64_t n_entries, uint32_t m,
+                        uint32_t k, int m_tb, int k_tb, const uint16_t* dX, int n, void* const* dPeerY, int n_peers,
+                        int out_dtype, const float* dBias, int activation, int split_k, int exact, void* ws,
+                        size_t ws_bytes, int* dErr, void* stream) {
+  if (n_peers <= 0 || n_peers > TCSL_MAX_PEERS || !dPeerY) return TCSL_STATUS_INVALID_ARGUMENT;
+  return spmm_core(dOffsets, dEntries, n_entries, m, k, m_tb, k_tb, dX, n, nullptr, out_dtype, dPeerY, n_peers,
+                   dBias, activation, split_k, exact, ws, ws_bytes, dErr, stream);
 }
 
 int tcsl_cuda_splitk_reduce(const float* dPartials, int split_k, size_t count, float* dY, void* stream) {

@@ -162,17 +162,28 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ p, int split, siz
 // epilogue of tcsl_cuda_spmm_ex; split == 1 is a pure epilogue pass.
 __global__ void reduce_epilogue_kernel(const float* __restrict__ p, int split, size_t count, int n,
                                        const float* __restrict__ bias, int act, float* __restrict__ y32,
-                                       uint16_t* __restrict__ y16) {
+                                       uint16_t* __restrict__ y16, void* const* __restrict__ peers, int n_peers,
+                                       int peers_f16) {
   griddep_wait();
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
     float acc = p[i];
     for (int s = 1; s < split; ++s) acc = __fadd_rn(acc, p[static_cast<size_t>(s) * count + i]);
     const float v = epilogue_value(acc, bias ? __ldg(bias + i / static_cast<size_t>(n)) : 0.0f, act);
-    if (y16)
+    if (n_peers > 0) {  // rows pushed to every peer's Y (NVLink stores for remote peers)
+      const uint32_t h = f16_bits_rne(v);
+      for (int g = 0; g < n_peers; ++g) {
+        void* base = peers[g];
+        if (peers_f16)
+          static_cast<uint16_t*>(base)[i] = static_cast<uint16_t>(h);
+        else
+          static_cast<float*>(base)[i] = v;
+      }
+    } else if (y16) {
       y16[i] = static_cast<uint16_t>(f16_bits_rne(v));
-    else
+    } else {
       y32[i] = v;
+    }
   }
 }
 
@@ -274,11 +285,13 @@ cudaError_t launch_splitk_reduce(const float* p, int split, size_t count, float*
 }
 
 cudaError_t launch_reduce_epilogue(const float* p, int split, uint32_t m, int n, const float* bias, int act,
-                                   float* y32, uint16_t* y16, cudaStream_t s) {
+                                   float* y32, uint16_t* y16, cudaStream_t s, void* const* peers, int n_peers,
+                                   bool peers_f16) {
   const size_t count = static_cast<size_t>(m) * n;
   if (count == 0) return cudaSuccess;
   const int blocks = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 8));
-  return launch_pdl(reduce_epilogue_kernel, blocks, 256, s, p, split, count, n, bias, act, y32, y16);
+  return launch_pdl(reduce_epilogue_kernel, blocks, 256, s, p, split, count, n, bias, act, y32, y16, peers,
+                    n_peers, peers_f16 ? 1 : 0);
 }
 
 cudaError_t launch_rebase(const uint32_t* off, uint32_t t0, uint32_t t1, uint32_t* out, cudaStream_t s) {

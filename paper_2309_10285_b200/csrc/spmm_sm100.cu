@@ -198,6 +198,8 @@ struct Params {
   int act;            // TCSL_ACT_* (split == 1)
   int out_f16;
   int ldo;
+  void* const* peers;  // fused all-gather (split == 1): Y rows to every peers[g] instead of out / out16
+  int n_peers;
   int* err;
   unsigned long long* trace;  // TCSL_TRACE builds only: per-event clock64 stamps of CTA 0
   int dbg;                    // ablation switches (see DBG)
@@ -469,7 +471,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, const Smem& s, uint
   PROF_ADD(5);
   if (tw == 0 && lane == 0) {
     TRACE(1, gt);
-    asm volatile("red.relaxed.cta.shared::cta.add.u32 [%0], 1;" ::"r"(s.done) : "memory");  // meta slot read
+    asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(s.done) : "memory");  // meta slot read (release: the slot may be rewritten)
   }
   if (!DBG(1)) scatter_groups<KG, TM::kZeroFill ? 1 : KG, !TM::kZeroFill>(E, Z, ncnt, a_tile);
   nz = DBG(1) ? 0 : ncnt;
@@ -680,17 +682,22 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__((Roles<TM, I>::kMaxRegs))
         const int ncol = min(C::kN, p.n - p.col0);
         const bool fused = p.bias != nullptr || p.act != 0 || p.out_f16;  // split == 1 only (host)
         const float b_row = (p.bias != nullptr && row_ok) ? __ldg(p.bias + row) : 0.0f;
+        // destinations: this CTA's Y, or (fused all-gather, split == 1) the same rows
+        // of every peer's Y, stored over NVLink for remote peers
+        const int ndst = p.n_peers > 0 ? p.n_peers : 1;
 #pragma unroll
         for (int c0 = 0; c0 < C::kN; c0 += 16) {
           uint32_t r[16];
           tmem_ld16_sum<I, 2 * C::kN>(t_base + c0, imask, r);
-          if (row_ok && fused) {
-            // fused epilogue: act(acc + bias) in fp32, optionally narrowed RNE to binary16
-            float v[16];
+          if (!row_ok) continue;
+          float v[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = epilogue_value(__uint_as_float(r[j]), b_row, p.act);
+          for (int j = 0; j < 16; ++j)
+            v[j] = fused ? epilogue_value(__uint_as_float(r[j]), b_row, p.act) : __uint_as_float(r[j]);
+          for (int g = 0; g < ndst; ++g) {
             if (p.out_f16) {
-              uint16_t* d16 = p.out16 + row * p.ldo + p.col0 + c0;
+              // act(acc + bias) in fp32, narrowed RNE to binary16
+              uint16_t* d16 = (p.n_peers > 0 ? static_cast<uint16_t*>(p.peers[g]) : p.out16) + row * p.ldo + p.col0 + c0;
               if (c0 + 16 <= ncol && ((reinterpret_cast<uintptr_t>(d16) & 15u) == 0)) {
                 uint32_t h[8];
 #pragma unroll
@@ -703,21 +710,16 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__((Roles<TM, I>::kMaxRegs))
                   if (c0 + j < ncol) d16[j] = static_cast<uint16_t>(f16_bits_rne(v[j]));
               }
             } else {
+              float* d = (p.n_peers > 0 ? static_cast<float*>(p.peers[g]) + row * p.ldo + p.col0 : dst) + c0;
+              if (c0 + 16 <= ncol && ((reinterpret_cast<uintptr_t>(d) & 15u) == 0)) {
+                float4* d4 = reinterpret_cast<float4*>(d);
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (c0 + j < ncol) dst[c0 + j] = v[j];
-            }
-          } else if (row_ok) {
-            if (c0 + 16 <= ncol && ((reinterpret_cast<uintptr_t>(dst + c0) & 15u) == 0)) {
-              float4* d4 = reinterpret_cast<float4*>(dst + c0);
+                for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              } else {
 #pragma unroll
-              for (int j = 0; j < 4; ++j)
-                d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                    __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (c0 + j < ncol) dst[c0 + j] = __uint_as_float(r[j]);
+                for (int j = 0; j < 16; ++j)
+                  if (c0 + j < ncol) d[j] = v[j];
+              }
             }
           }
         }
@@ -1246,7 +1248,9 @@ cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const u
   p.units = plan.units;
   p.out = out;
   p.out16 = epi.out16;
-  p.out_f16 = epi.out16 != nullptr;
+  p.out_f16 = epi.out16 != nullptr || (epi.n_peers > 0 && epi.peers_f16);
+  p.peers = epi.peers;
+  p.n_peers = epi.n_peers;
   p.bias = epi.bias;
   p.act = epi.act;
   p.ldo = plan.n;

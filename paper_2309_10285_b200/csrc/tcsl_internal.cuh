@@ -89,8 +89,11 @@ cudaError_t launch_dense_gemm_exact(const uint16_t* a, uint32_t m, uint32_t k, c
 cudaError_t launch_splitk_reduce(const float* p, int split, size_t count, float* y, cudaStream_t s);
 // Split-K reduce (or, split == 1, a pure epilogue pass) with the fused epilogue:
 // y[i] = act(sum_s p[s][i] + bias[i / n]) as fp32 (y32) or binary16 (y16).
+// peers / n_peers > 0: the result goes to n_peers destinations (device array of
+// base pointers, each laid out like y32 / y16) instead of y32 / y16.
 cudaError_t launch_reduce_epilogue(const float* p, int split, uint32_t m, int n, const float* bias, int act,
-                                   float* y32, uint16_t* y16, cudaStream_t s);
+                                   float* y32, uint16_t* y16, cudaStream_t s, void* const* peers = nullptr,
+                                   int n_peers = 0, bool peers_f16 = false);
 // tcsl_cuda_prune_magnitude (prune.cu)
 size_t prune_workspace_bytes(uint64_t count);
 cudaError_t launch_prune(const uint16_t* a, uint64_t count, uint64_t cut, uint16_t* out, void* ws, size_t ws_bytes,
@@ -112,6 +115,9 @@ struct Epilogue {
   const float* bias = nullptr;  // per row
   int act = 0;                  // TCSL_ACT_*
   uint16_t* out16 = nullptr;    // binary16 output instead of fp32
+  void* const* peers = nullptr;  // > 0 peers: Y rows go to every peers[g] (device array) instead of out
+  int n_peers = 0;
+  bool peers_f16 = false;        // the peers' dtype (binary16 or fp32)
 };
 cudaError_t launch_spmm_sm100(const SpmmPlan& plan, const uint32_t* off, const uint32_t* ent,
                               uint64_t n_entries, uint32_t m, uint32_t k, const uint16_t* x, int ldx,

@@ -9,6 +9,12 @@ Tiled-CSL that `encode` would produce for those rows (checked in the tests).
 X is replicated; each rank computes its rows of Y, and one all-gather (NCCL
 over NVLink on GPUs, gloo on CPU) assembles Y in rank order. No other
 collective exists on this path.
+
+Fused alternative (push=True): Y lives in symmetric memory (one full-Y buffer
+per rank, peer-mapped over NVLink); the SpMM epilogue stores every finished
+row block straight into all ranks' buffers (tcsl_cuda_spmm_push), so the
+exchange overlaps the SpMM tile by tile and only a device-side barrier
+(symmetric-memory signal pads) follows the kernel.
 """
 from __future__ import annotations
 
@@ -84,23 +90,61 @@ def allgather_rows(y_local, plan: list[Shard], group=None, comm=None, out=None):
     return torch.cat(parts, dim=0)
 
 
+def push_targets(buffer_ptrs, plan: list[Shard], rank: int, n: int, elem_bytes: int) -> list[int]:
+    """Device addresses the fused epilogue writes rank `rank`'s rows to: its row
+    block (rank * rmax rows in) inside every rank's full-Y buffer (rank-major,
+    rmax rows per rank, row stride n)."""
+    rmax = max_rows(plan)
+    return [int(p) + rank * rmax * n * elem_bytes for p in buffer_ptrs]
+
+
 class RowShardedSpmm:
     """One rank's part of a row-sharded SpMM on the GPU: holds the rank's
-    Tiled-CSL shard (device), runs the tcgen05 SpMM on it and all-gathers Y."""
+    Tiled-CSL shard (device), runs the tcgen05 SpMM on it and all-gathers Y —
+    after the kernel (NCCL / torch.distributed), or fused into its epilogue
+    (push=True: symmetric-memory Y, tcsl_cuda_spmm_push, device barrier)."""
 
-    def __init__(self, t_full, world: int, rank: int, group=None, comm=None):
+    def __init__(self, t_full, world: int, rank: int, group=None, comm=None, push: bool = False):
         from . import shard_rows
         self.plan = shard_plan(t_full.m, t_full.cfg.m_tb, world)
         self.shard = self.plan[rank]
+        self.rank = rank
         self.group = group
         self.comm = comm  # RowComm: the C-ABI NCCL all-gather (else torch.distributed)
+        self.push = push
+        self._symm = {}  # (n, dtype) -> (full-Y symmetric buffer, handle, device peer table)
         self.local = shard_rows(t_full, self.shard.tr0, self.shard.tr1) if self.shard.rows else None
         self.m = t_full.m
+
+    def _push_buffer(self, n, dtype, device):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        key = (n, dtype)
+        if key not in self._symm:
+            rmax = max_rows(self.plan)
+            y = symm_mem.empty(len(self.plan) * rmax, n, dtype=dtype, device=device)
+            group = self.group or dist.group.WORLD
+            h = symm_mem.rendezvous(y, group)
+            ptrs = push_targets(h.buffer_ptrs, self.plan, self.rank, n, y.element_size())
+            self._symm[key] = (y, h, torch.tensor(ptrs, dtype=torch.int64, device=device))
+        return self._symm[key]
 
     def __call__(self, x, split_k: int = 0, out_dtype=None):
         import torch
 
-        from . import spmm
+        from . import spmm, spmm_push
+        if self.push:
+            dtype = out_dtype or torch.float32
+            y, h, peers = self._push_buffer(x.shape[1], dtype, x.device)
+            h.barrier(channel=0)  # every rank is done reading the previous result
+            if self.local is not None:
+                spmm_push(self.local, x, peers, split_k=split_k, out_dtype=dtype)
+            h.barrier(channel=0)  # every rank's rows have landed in every buffer
+            if all(sh.rows == max_rows(self.plan) for sh in self.plan):
+                return y
+            rmax = max_rows(self.plan)
+            return torch.cat([y[sh.rank * rmax: sh.rank * rmax + sh.rows] for sh in self.plan], dim=0)
         if self.local is not None:
             y = spmm(self.local, x, split_k=split_k, out_dtype=out_dtype)
         else:

@@ -73,3 +73,25 @@ def test_shard_plan_covers_rows():
             assert sum(s.rows for s in plan) == m
             assert all(s.row0 == s.tr0 * 128 for s in plan)
             assert [s.tr1 for s in plan[:-1]] == [s.tr0 for s in plan[1:]]
+
+
+@pytest.mark.parametrize("world,m", [(2, 49152), (8, 49152), (3, 1000), (4, 300)])
+def test_push_targets_tile_the_buffer(world, m):
+    """Fused all-gather addressing (sharding.push_targets): rank r's rows land at
+    r * rmax rows into every rank's full-Y buffer; over all ranks the written row
+    ranges are disjoint, in rank order, and cover every real row once."""
+    from paper_2309_10285_b200.sharding import max_rows, push_targets
+    plan = shard_plan(m, 128, world)
+    n, eb = 32, 4
+    bases = [1 << 40, 2 << 40, 3 << 40][:1] * world
+    rmax = max_rows(plan)
+    covered = []
+    for sh in plan:
+        t = push_targets([bases[0]] * world, plan, sh.rank, n, eb)
+        assert len(t) == world and len(set(t)) == 1
+        row0 = (t[0] - bases[0]) // (n * eb)
+        assert row0 == sh.rank * rmax
+        covered.append((row0, row0 + sh.rows))
+    for (a0, a1), (b0, b1) in zip(covered, covered[1:]):
+        assert a1 <= b0
+    assert sum(b - a for a, b in covered) == m
