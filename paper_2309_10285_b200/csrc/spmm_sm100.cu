@@ -568,31 +568,36 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__((Roles<TM, I>::kMaxRegs))
 #ifdef TCSL_TRACE
     if (p.trace) p.trace[16 * 4096 + blockIdx.x] = globaltimer_ns();  // every CTA: start (ns)
 #endif
-    for (int i = 0; i < kNB; ++i) mbar_init(s.cfull + 8 * i, 1);
-    for (int i = 0; i < C::kNR; ++i) mbar_init(s.cempty + 8 * i, 1);
-    for (int i = 0; i < TM::kNA; ++i) {
+  }
+  if (warp == 0) {
+    // ~100 mbarriers, spread over the lanes of warp 0 (one thread initialising them
+    // in sequence is ~2 K cycles of the prologue)
+    for (int i = lane; i < kNB; i += 32) mbar_init(s.cfull + 8 * i, 1);
+    if (lane < C::kNR) mbar_init(s.cempty + 8 * lane, 1);
+    for (int i = lane; i < TM::kNA; i += 32) {
       if (i < TM::kNP) {
         mbar_init(s.afull + 8 * i, TM::kG * 2 * TM::kTeamWarps);
         mbar_init(s.aempty + 8 * i, 1);
       }
       st_shared_u32(s.ovf + 4 * i, 0xFFFFFFFFu);
     }
-    for (int i = 0; i < NX; ++i) {
-      mbar_init(s.xfull + 8 * i, 2);
-      mbar_init(s.xempty + 8 * i, 1);
+    if (lane < NX) {
+      mbar_init(s.xfull + 8 * lane, 2);
+      mbar_init(s.xempty + 8 * lane, 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(s.dfull + 8 * i, I);
-      mbar_init(s.dempty + 8 * i, 8);
+    if (lane < 2) {
+      mbar_init(s.dfull + 8 * lane, I);
+      mbar_init(s.dempty + 8 * lane, 8);
     }
-    st_shared_u32(s.tiles_ready, 0u);
-    st_shared_u32(s.done, 0u);
-    st_shared_u32(s.tab_ready, 0u);
+    if (lane == 0) {
+      st_shared_u32(s.tiles_ready, 0u);
+      st_shared_u32(s.done, 0u);
+      st_shared_u32(s.tab_ready, 0u);
+    }
     fence_barrier_init();
   }
   if (warp == TM::kWarpX && lane == 0) prefetch_tmap(&tmap_x);
   if (warp == TM::kWarpMma) tmem_alloc_pair(s.tmem_slot, C::kTmemCols);
-  for (uint32_t i = threadIdx.x; i < TM::kNA * kABytes / 16; i += Roles<TM, I>::kThreads) sts128_zero(s.a + 16 * i);
   // Programmatic dependent launch: everything above touches only this CTA's smem,
   // TMEM and parameters, so it overlaps the tail of the previous kernel in the
   // stream; global memory is read and written only after the previous grid has
@@ -642,6 +647,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__((Roles<TM, I>::kMaxRegs))
     const long long prof_start = clock64();
 #endif
     PROF_MARK();
+    // the team's dense-tile buffer starts zeroed (the first tile neither clears nor
+    // zero-fills); done here, while the first ring chunk is in flight, rather than in
+    // the prologue every role waits for. The team barrier in decode_tile orders it
+    // before the first scatter.
+    if (static_cast<uint32_t>(team) < total)
+      for (uint32_t r = tw; r < kABytes / 512; r += TM::kTeamWarps) sts128_zero(s.a + team * kABytes + 512 * r + 16 * lane);
     for (uint32_t gt = team; gt < total; gt += TM::kTeams)
       decode_tile<TM, C::kRing>(p, s, gt, team, tw, lane, afull_leader, total, E, Z, nz, err_or, prof_);
 #ifdef TCSL_PROFILING
