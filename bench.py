@@ -419,6 +419,9 @@ def run_ours(args, rank, world):
                           "split": args.split or tc.auto_split(t.m, t.k, n), "us": round(us, 2),
                           "tflops": round(fl / us / 1e6, 2), "gbs": round(nbytes / us / 1e3, 1),
                           "hbm_frac": round(t_hbm / us, 3), "roofline_frac": round(max(t_hbm, t_tc) / us, 3)})
+        est = tc.estimate(t.m, t.k, n, t.n_entries, cell_rows[-1]["split"], hbm_peak)
+        cell_rows[-1]["model_us"] = round(est["us"], 2)
+        cell_rows[-1]["model_bound"] = est["bound"]
         sum_t += us
         sum_bytes += nbytes
     torch.cuda.synchronize()
@@ -462,6 +465,13 @@ def run_ours(args, rank, world):
         "sum_cold_cell_ms": round(sum_t / 1e3, 4),
     }
     result["cells"] = cell_rows
+    rel = sorted(abs(r["model_us"] - r["us"]) / r["us"] for r in cell_rows)
+    result["model"] = {
+        "what": "a-priori B200 time model tcsl_cuda_spmm_estimate (fixed + max(HBM, tensor, smem, chain)) vs the "
+                "cold per-cell times",
+        "median_rel_err": round(rel[len(rel) // 2], 4), "max_rel_err": round(rel[-1], 4),
+        "bounds": {b: sum(r["model_bound"] == b for r in cell_rows) for b in ("hbm", "tensor", "smem", "chain")},
+    }
     result["encoder"] = {
         "kernel": "K1 tcsl_cuda_encode_count + scan + encode_emit (bit-exact Tiled-CSL)",
         "weights": len(enc), "ms_total": round(sum(v[0] for v in enc.values()) / 1e3, 3),

@@ -183,6 +183,25 @@ int tcsl_cuda_spmm_push(const uint32_t* dOffsets, const uint32_t* dEntries, uint
                         uint32_t k, int m_tb, int k_tb, const uint16_t* dX, int n, void* const* dPeerY, int n_peers,
                         int out_dtype, const float* dBias, int activation, int split_k, int exact, void* ws,
                         size_t ws_bytes, int* dErr, void* stream);
+/* A-priori time model of tcsl_cuda_spmm on a B200 (the B200 counterpart of the
+ * reference's estimate_time, proj/src/pipeline.cpp:214-273, which models the
+ * A100 kernel as max(gmem, smem, tensor) time): per persistent CTA,
+ *   t = fixed + max(HBM, tensor, smem, chain),
+ * HBM = (4E + 4(T+1) + 2KN + 4MN) / hbm_gbs (0: the measured 6558.7 GB/s);
+ * tensor = 4 tcgen05.mma per tile at the in-situ 32 cycles (ncu); smem = the
+ * shared-memory wavefronts of one tile (ring LDS, scatter, clear or zero fill,
+ * bulk-copy landing, tensor-core operand reads) at 1 per cycle; chain = the
+ * per-tile decode/issue handshake latency, 284 + 3.95 g + 0.76 N cycles for g
+ * groups per tile (fitted to the 84 cold cells of profiles/r02_bench_v3.json);
+ * fixed = 10.9 us per launch + 2.4 us for the split-K pass; clock 1965 MHz.
+ * split_k 0 = the auto choice. Host only (no GPU needed). */
+enum { TCSL_BOUND_HBM = 0, TCSL_BOUND_TENSOR = 1, TCSL_BOUND_SMEM = 2, TCSL_BOUND_CHAIN = 3 };
+typedef struct {
+  double us, hbm_us, tensor_us, smem_us, chain_us, fixed_us;
+  int split, bound;
+} tcsl_cuda_estimate;
+int tcsl_cuda_spmm_estimate(uint32_t m, uint32_t k, int n, uint64_t n_entries, int split_k, double hbm_gbs,
+                            tcsl_cuda_estimate* out);
 int tcsl_cuda_spmm_auto_split(uint32_t m, uint32_t k, int n);
 /* Y = sum_{s=0}^{S-1} P[s] in ascending s (P is S x count floats). */
 int tcsl_cuda_splitk_reduce(const float* dPartials, int split_k, size_t count, float* dY, void* stream);

@@ -116,6 +116,7 @@ def lib() -> C.CDLL:
         "tcsl_cuda_spmm_workspace": ([u32, u32, i32, i32, i32, i32, C.POINTER(sz)], i32),
         "tcsl_cuda_spmm": ([vp, vp, u64, u32, u32, i32, i32, vp, i32, vp, i32, vp, sz, vp, vp], i32),
         "tcsl_cuda_spmm_auto_split": ([u32, u32, i32], i32),
+        "tcsl_cuda_spmm_estimate": ([u32, u32, i32, u64, i32, C.c_double, C.POINTER(Estimate)], i32),
         "tcsl_cuda_splitk_reduce": ([vp, i32, sz, vp, vp], i32),
         "tcsl_cuda_spmm_exact_workspace": ([u32, u32, C.POINTER(sz)], i32),
         "tcsl_cuda_spmm_exact": ([vp, vp, u64, u32, u32, i32, i32, vp, i32, vp, vp, sz, vp, vp], i32),
@@ -155,12 +156,14 @@ def lib() -> C.CDLL:
 EXPORTED_SYMBOLS = [
     "tcsl_cuda_abi_version", "tcsl_cuda_status_string", "tcsl_cuda_last_cuda_error", "tcsl_cuda_read_error",
     "tcsl_cuda_encode_workspace", "tcsl_cuda_encode_count", "tcsl_cuda_encode_emit", "tcsl_cuda_decode",
-    "tcsl_cuda_encode_fused_workspace", "tcsl_cuda_encode_fused", "tcsl_cuda_validate", "tcsl_cuda_spmm_workspace", "tcsl_cuda_spmm", "tcsl_cuda_spmm_auto_split",
+    "tcsl_cuda_encode_fused_workspace", "tcsl_cuda_encode_fused", "tcsl_cuda_validate", "tcsl_cuda_spmm_workspace",
+    "tcsl_cuda_spmm", "tcsl_cuda_spmm_auto_split", "tcsl_cuda_spmm_estimate",
     "tcsl_cuda_splitk_reduce", "tcsl_cuda_spmm_exact_workspace", "tcsl_cuda_spmm_exact",
     "tcsl_cuda_rebase_offsets", "tcsl_cuda_gen_synthetic", "tcsl_cuda_malloc", "tcsl_cuda_free",
     "tcsl_cuda_memcpy_h2d", "tcsl_cuda_memcpy_d2h", "tcsl_cuda_memset", "tcsl_cuda_stream_sync",
     "tcsl_cuda_device_count", "tcsl_cuda_validate_entries", "tcsl_cuda_parse_header", "tcsl_cuda_ingest",
-    "tcsl_cuda_spmm_ex_workspace", "tcsl_cuda_spmm_ex", "tcsl_cuda_spmm_push", "tcsl_cuda_prune_workspace", "tcsl_cuda_prune_magnitude",
+    "tcsl_cuda_spmm_ex_workspace", "tcsl_cuda_spmm_ex", "tcsl_cuda_spmm_push", "tcsl_cuda_prune_workspace",
+    "tcsl_cuda_prune_magnitude",
     "tcsl_cuda_nccl_available", "tcsl_cuda_nccl_unique_id", "tcsl_cuda_nccl_comm_init",
     "tcsl_cuda_nccl_comm_destroy", "tcsl_cuda_allgather_rows",
 ]
@@ -467,6 +470,23 @@ def spmm_push(t: TcslMatrix, x, peer_ptrs, split_k: int = 0, exact: bool = False
                                  _ptr(err), s), "spmm")
     if check:
         _check(L.tcsl_cuda_read_error(_ptr(err), s), "spmm")
+
+
+class Estimate(C.Structure):
+    _fields_ = [("us", C.c_double), ("hbm_us", C.c_double), ("tensor_us", C.c_double), ("smem_us", C.c_double),
+                ("chain_us", C.c_double), ("fixed_us", C.c_double), ("split", C.c_int), ("bound", C.c_int)]
+
+
+BOUNDS = ("hbm", "tensor", "smem", "chain")
+
+
+def estimate(m: int, k: int, n: int, n_entries: int, split_k: int = 0, hbm_gbs: float = 0.0) -> dict:
+    """A-priori B200 time of spmm (tcsl_cuda_spmm_estimate; the B200 counterpart of
+    the reference's estimate_time, proj/src/pipeline.cpp:214-273). Host only."""
+    e = Estimate()
+    _check(lib().tcsl_cuda_spmm_estimate(m, k, n, n_entries, split_k, float(hbm_gbs), C.byref(e)), "estimate")
+    return {"us": e.us, "hbm_us": e.hbm_us, "tensor_us": e.tensor_us, "smem_us": e.smem_us,
+            "chain_us": e.chain_us, "fixed_us": e.fixed_us, "split": e.split, "bound": BOUNDS[e.bound]}
 
 
 def auto_split(m: int, k: int, n: int) -> int:

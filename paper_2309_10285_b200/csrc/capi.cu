@@ -327,6 +327,40 @@ int tcsl_cuda_prune_magnitude(const uint16_t* dA, uint64_t count, double beta, u
 // -------------------------------------------------------------------- spmm
 int tcsl_cuda_spmm_auto_split(uint32_t m, uint32_t k, int n) { return effective_split(m, k, n, 0); }
 
+int tcsl_cuda_spmm_estimate(uint32_t m, uint32_t k, int n, uint64_t n_entries, int split_k, double hbm_gbs,
+                            tcsl_cuda_estimate* out) {
+  if (!out || m == 0 || k == 0 || n <= 0 || split_k < 0) return TCSL_STATUS_INVALID_ARGUMENT;
+  constexpr double kClockMHz = 1965.0;     // B200 SM clock under load (bench clocks)
+  constexpr double kMmaCycles = 32.0;      // per tcgen05.mma M=256 instruction, in situ (ncu)
+  constexpr double kChain0 = 284.3, kChainG = 3.95, kChainN = 0.763;  // cycles per tile (fit)
+  constexpr double kFixedUs = 10.89, kSplitUs = 2.42;                  // per launch, split-K pass (fit)
+  if (hbm_gbs <= 0) hbm_gbs = 6558.7;      // MEASURED_PEAKS.json copy bandwidth
+  const uint32_t tiles_m = (m + 127) / 128, tiles_k = (k + 63) / 64;
+  const double tiles = static_cast<double>(tiles_m) * tiles_k;
+  const int split = effective_split(m, k, n, split_k);
+  const int clusters = std::max(1, tcslk::num_sms() / 2);
+  const uint64_t units = static_cast<uint64_t>((tiles_m + 1) / 2) * split;
+  const double per_cta = static_cast<double>((units + clusters - 1) / clusters) *
+                         static_cast<double>((tiles_k + split - 1) / split);
+  const double g = static_cast<double>(n_entries) / 32.0 / tiles;
+  const double clear = g <= 32.0 ? 1.5 * g : (g <= 81.0 ? 128.0 : 1.5 * g);  // rescatter or zero fill
+  const double wavefronts = g * (1.0 + 1.5) + clear + 136.0 + 4.0 * n_entries / tiles / 128.0;
+  const double bytes = 4.0 * n_entries + 4.0 * (tiles + 1) + 2.0 * k * n + 4.0 * static_cast<double>(m) * n;
+  out->split = split;
+  out->hbm_us = bytes / (hbm_gbs * 1e3);
+  out->tensor_us = per_cta * 4.0 * kMmaCycles / kClockMHz;
+  out->smem_us = per_cta * wavefronts / kClockMHz;
+  out->chain_us = per_cta * (kChain0 + kChainG * g + kChainN * n) / kClockMHz;
+  out->fixed_us = kFixedUs + (split > 1 ? kSplitUs : 0.0);
+  double worst = out->hbm_us;
+  out->bound = TCSL_BOUND_HBM;
+  if (out->tensor_us > worst) { worst = out->tensor_us; out->bound = TCSL_BOUND_TENSOR; }
+  if (out->smem_us > worst) { worst = out->smem_us; out->bound = TCSL_BOUND_SMEM; }
+  if (out->chain_us > worst) { worst = out->chain_us; out->bound = TCSL_BOUND_CHAIN; }
+  out->us = out->fixed_us + worst;
+  return TCSL_STATUS_OK;
+}
+
 int tcsl_cuda_spmm_exact_workspace(uint32_t m, uint32_t k, size_t* ws_bytes) {
   if (!ws_bytes) return TCSL_STATUS_INVALID_ARGUMENT;
   *ws_bytes = align256(static_cast<size_t>(m) * k * 2);
