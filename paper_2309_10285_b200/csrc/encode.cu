@@ -526,8 +526,11 @@ __device__ __forceinline__ void load_tile128(const uint16_t* __restrict__ w, uin
 // four per-column counts of a lane pack into the bytes of one register and a
 // single byte-packed warp scan per slice gives every element's FIFO index
 // (lane order inside a slice is row-major, slices are in row order).
+#ifndef TCSL_EMIT_MINB
+#define TCSL_EMIT_MINB 6  // 40 registers, 6 blocks per SM (the 36 KB smem limit): 386 us vs 392 (5) and 409 (4)
+#endif
 template <bool FUSED>
-__global__ void __launch_bounds__(256, 5) encode_emit128_kernel(const uint16_t* __restrict__ w, uint32_t m,
+__global__ void __launch_bounds__(256, TCSL_EMIT_MINB) encode_emit128_kernel(const uint16_t* __restrict__ w, uint32_t m,
                                                                  uint32_t k, int tiles_k, uint32_t tiles,
                                                                  const uint32_t* __restrict__ offsets_in,
                                                                  uint32_t* __restrict__ offsets_out,
