@@ -134,7 +134,10 @@ using TeamsDense3 = Teams<8, 3, 1, 28, true>;
 
 
 constexpr uint32_t kRingMin = 65536;           // entry ring bytes (power of two; Cfg::kRing may be larger)
-constexpr uint32_t kChunk = 16384;             // bytes per bulk copy (>= 8 KB: ~7 TB/s, profiles/r01_bulk_copy_bench.txt)
+#ifndef TCSL_CHUNK
+#define TCSL_CHUNK 16384
+#endif
+constexpr uint32_t kChunk = TCSL_CHUNK;             // bytes per bulk copy (>= 8 KB: ~7 TB/s, profiles/r01_bulk_copy_bench.txt)
 // "chunk landed" barriers: chunk k uses cfull[k % kNB]. A decoder may wait for a
 // chunk up to ~9 tiles (<= 45 chunks) past the oldest unconsumed one; with more
 // barriers than that, the barrier's previous phase is always complete, so the
