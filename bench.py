@@ -45,6 +45,7 @@ SUITES = {
             "(84 per step)"),
     "opt66b": (SHAPES_66B, "OPT-66B QKV/out/FFN1/FFN2 SpMMs x N{8,16,32,64} x sparsity{0.7,0.8,0.9} (48 per step)"),
     "opt175b": (SHAPES_175B, "OPT-175B QKV/FFN1/FFN2 SpMMs x N{8,16,32,64} x sparsity{0.7,0.8,0.9} (36 per step)"),
+    "c1": ({"c1": (7168, 7168)}, "OPT-30B attn-out 7168x7168 (configs[0]; use --only c1:0.8:16)"),
 }
 SHAPES, WORKLOAD = SUITES["all"]
 NS = [8, 16, 32, 64]
@@ -669,7 +670,7 @@ def main():
     args = ap.parse_args()
     SHAPES, WORKLOAD = SUITES[args.suite]
     if args.only:
-        SHAPES = {**SHAPES_66B, **SHAPES_175B}
+        SHAPES = {**SHAPES_66B, **SHAPES_175B, **SUITES["c1"][0]}
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
