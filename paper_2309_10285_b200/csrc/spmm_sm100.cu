@@ -118,12 +118,6 @@ struct Roles {
 // waiting on aempty itself (A/B builds only).
 constexpr bool kPollRelease = TCSL_POLL_RELEASE;
 using TeamsSparse = Teams<8, 2, TCSL_SPARSE_G>;  // G=1, per-tile release: +2-5 % over G=2 (r01_ablation_mma_loop)
-#ifndef TCSL_SPARSE3_KG
-#define TCSL_SPARSE3_KG 12
-#endif
-// A/B: 8 teams of 3 warps for sparse tiles (2/3 of the groups per warp; 32 warps
-// with one MMA issuer is the 1024-thread limit)
-using TeamsSparse3 = Teams<8, 3, 1, TCSL_SPARSE3_KG, false>;
 #ifndef TCSL_DENSE_T
 #define TCSL_DENSE_T 6
 #endif
@@ -1186,8 +1180,6 @@ template <int NH>
 cudaError_t launch_nh(const Params& p, const CUtensorMap& tm, int clusters, cudaStream_t s) {
   const uint64_t tiles = static_cast<uint64_t>(p.tiles_m) * p.tiles_k;
   const int env = issuers_env();
-  static const bool sparse3 = getenv("TCSL_SPARSE3") && atoi(getenv("TCSL_SPARSE3")) != 0;
-  if (sparse3 && sparse_teams(p.n_entries, tiles)) return launch_iss<NH, TeamsSparse3>(p, tm, clusters, s, 1);
   if (sparse_teams(p.n_entries, tiles)) return launch_iss<NH, TeamsSparse>(p, tm, clusters, s, env ? env : 2);
   if (dense3_teams(p.n_entries, tiles)) return launch_iss<NH, TeamsDense3>(p, tm, clusters, s, env ? env : 1);
   return launch_iss<NH, TeamsDense>(p, tm, clusters, s, env ? env : 1);
