@@ -10,7 +10,11 @@ for line in sys.stdin:
         continue
     m = re.search(r"(\d+) bytes stack frame, (\d+) bytes spill stores, (\d+) bytes spill loads", line)
     if m and cur and "spmm_sm100_kernel" in cur:
-        t = re.search(r"spmm_sm100_kernelILi(\d+)ENS0_5TeamsILi(\d)ELi(\d)ELi(\d)ELi(\d+)ELb([01])EEELi(\d)", cur)
-        print("NH=%s T=%s W=%s KG=%s ZF=%s I=%s" % (t.group(1), t.group(2), t.group(3), t.group(5), t.group(6), t.group(7)),
+        nh = re.search(r"spmm_sm100_kernelILi(\d+)E", cur).group(1)
+        teams = re.search(r"TeamsILi(\d)ELi(\d)ELi(\d)ELi(\d+)E((?:Lb[01]E)+)", cur)
+        flags = re.findall(r"Lb([01])E", teams.group(5))
+        iss = re.search(r"EEELi(\d)EEEv", cur)
+        print("NH=%s T=%s W=%s KG=%s flags=%s I=%s" % (nh, teams.group(1), teams.group(2), teams.group(4),
+                                                       "".join(flags), iss.group(1) if iss else "?"),
               "stack", m.group(1), "spill st/ld", m.group(2), m.group(3))
         cur = None
