@@ -417,9 +417,12 @@ __device__ __forceinline__ void sts_u32_if(uint32_t addr, uint32_t v, uint32_t p
                "r"(pred)
                : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+// The look-back status word is self-contained (flag and value in one 64-bit word,
+// nothing else published through it), so relaxed loads suffice; an acquire load
+// would hold back the warp's later shared-memory work until it completes.
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsigned long long v) {
@@ -597,34 +600,9 @@ __global__ void __launch_bounds__(256, TCSL_EMIT_MINB) encode_emit128_kernel(con
       const uint32_t mk = __ballot_sync(0xffffffffu, cl >= L);
       if (lane == 0) s_tab[L] = make_uint2(f, mk);
     }
-    if (FUSED && warp == 0) {
-      // decoupled look-back
-      if (lane == 0) st_release_gpu_u64(status + tile, (tile == 0 ? kPrefix : kAggregate) | total);
-      uint32_t acc = 0;
-      for (long long jt = static_cast<long long>(tile) - 1; jt >= 0; jt -= 32) {
-        const long long idx = jt - lane;
-        unsigned long long sv = 0;
-        if (idx >= 0) {
-          do {
-            sv = ld_acquire_gpu_u64(status + idx);
-          } while ((sv >> 32) == 0);
-        }
-        const uint32_t pm = __ballot_sync(0xffffffffu, idx >= 0 && (sv >> 32) == 2);
-        const uint32_t val = idx >= 0 ? static_cast<uint32_t>(sv) : 0u;
-        if (pm) {
-          const int f = __ffs(pm) - 1;
-          acc += __reduce_add_sync(0xffffffffu, lane <= f ? val : 0u);
-          break;
-        }
-        acc += __reduce_add_sync(0xffffffffu, val);
-      }
-      if (lane == 0) {
-        if (tile) st_release_gpu_u64(status + tile, kPrefix | (acc + total));
-        offsets_out[tile + 1] = acc + total;
-        if (tile == 0) offsets_out[0] = 0;
-        s_misc[1] = acc;
-      }
-    }
+    // one pass: publish this tile's count now; the look-back for its base runs after
+    // the place phase, when the earlier tiles have had that time to publish prefixes
+    if (FUSED && warp == 0 && lane == 0) st_release_gpu_u64(status + tile, (tile == 0 ? kPrefix : kAggregate) | total);
     uint32_t base = 0;
     if (!FUSED) {
       base = offsets_in[tile];
@@ -634,7 +612,6 @@ __global__ void __launch_bounds__(256, TCSL_EMIT_MINB) encode_emit128_kernel(con
       }
     }
     __syncthreads();  // (2)
-    if (FUSED) base = s_misc[1];
 
     // ---- +0.0 pads at the first `pad` zero positions, row-major (fringe included)
     if (pad && warp == 7) {
@@ -678,7 +655,33 @@ __global__ void __launch_bounds__(256, TCSL_EMIT_MINB) encode_emit128_kernel(con
         sts_u32_if(stg + 4u * (t1.x + __popc(t1.y & below)), __byte_perm(r, loc0 + 1u, 0x3254), nb >> 31);
       }
     }
+    if (FUSED && warp == 0) {
+      // decoupled look-back
+      uint32_t acc = 0;
+      for (long long jt = static_cast<long long>(tile) - 1; jt >= 0; jt -= 32) {
+        const long long idx = jt - lane;
+        unsigned long long sv = 0;
+        if (idx >= 0) {
+          while ((sv >> 32) == 0) sv = ld_relaxed_gpu_u64(status + idx);
+        }
+        const uint32_t pm = __ballot_sync(0xffffffffu, idx >= 0 && (sv >> 32) == 2);
+        const uint32_t val = idx >= 0 ? static_cast<uint32_t>(sv) : 0u;
+        if (pm) {
+          const int f = __ffs(pm) - 1;
+          acc += __reduce_add_sync(0xffffffffu, lane <= f ? val : 0u);
+          break;
+        }
+        acc += __reduce_add_sync(0xffffffffu, val);
+      }
+      if (lane == 0) {
+        if (tile) st_release_gpu_u64(status + tile, kPrefix | (acc + total));
+        offsets_out[tile + 1] = acc + total;
+        if (tile == 0) offsets_out[0] = 0;
+        s_misc[1] = acc;
+      }
+    }
     __syncthreads();  // (3)
+    if (FUSED) base = s_misc[1];
     if (!FUSED || static_cast<uint64_t>(base) + total <= capacity) {  // else the host sees offsets[T] > capacity
       uint4* dst = reinterpret_cast<uint4*>(entries + base);
       const uint4* src = reinterpret_cast<const uint4*>(s_stg);
