@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "tcsl/device.hpp"
 #include "tcsl/engine.hpp"
 #include "tcsl/gemm.hpp"
 #include "tcsl/tcsl_format.hpp"
@@ -150,58 +151,101 @@ std::vector<HalfBits> extract_tile(const TcslMatrix& t, std::uint32_t tile) {
 
 FloatMatrix spmm(const TcslMatrix& a, const HalfMatrix& b) { return spmm(a, b, SpmmOptions{}); }
 
-FloatMatrix spmm(const TcslMatrix& a, const HalfMatrix& b, const SpmmOptions& opt) {
+namespace {
+
+// Argument checks of tcsl::spmm (engine.cpp:28-32) and extract_tile's per-tile
+// spans (engine.cpp:11-14) on the host copy of the offsets.
+void check_spmm_args(const TcslMatrix& a) {
   a.cfg.validate();
-  if (b.rows() <= 0 || b.cols() <= 0) raise(Errc::invalid_argument, "B must be non-empty");
-  if (static_cast<std::int64_t>(a.k) != b.rows())
-    raise(Errc::dimension_mismatch,
-          "A has " + std::to_string(a.k) + " columns, B has " + std::to_string(b.rows()) + " rows");
   if (a.tile_offsets.size() != static_cast<std::size_t>(a.num_tiles()) + 1)
     raise(Errc::inconsistent_offsets, "offset table does not match tile count");
   for (std::uint32_t t = 0; t < a.num_tiles(); ++t)  // the per-tile checks of extract_tile (engine.cpp:11-14)
     if (a.tile_offsets[t + 1] < a.tile_offsets[t] || a.tile_offsets[t + 1] > a.entries.size())
       raise(Errc::inconsistent_offsets, "offset table does not match entries");
+}
+
+// The reference accepts tiles whose spans are not whole 32-entry groups and
+// locations repeated inside a tile (last writer wins, engine.cpp:8-25); the
+// tensor-core decoders need neither. One device pass over the uploaded entries
+// finds out; such matrices take the bit-exact path, which handles both.
+bool tc_preconditions(const std::uint32_t* off, const std::uint32_t* ent, std::uint64_t n_entries, std::uint32_t m,
+                      std::uint32_t k, const TileConfig& cfg) {
+  if (cfg.m_tb != 128 || cfg.k_tb != 64) return false;
+  auto* flags = static_cast<std::uint32_t*>(scratch().flags.get(sizeof(std::uint32_t)));
+  check(tcsl_cuda_memset(flags, 0, sizeof(std::uint32_t), nullptr), "memset");
+  int* verr = fresh_error_word();
+  check(tcsl_cuda_validate_entries(off, ent, n_entries, m, k, cfg.m_tb, cfg.k_tb, TCSL_CHECK_SPMM, flags, verr,
+                                   nullptr),
+        "spmm");
+  std::uint32_t h = 0;
+  check(tcsl_cuda_memcpy_d2h(&h, flags, sizeof h, nullptr), "spmm");
+  collect_errors(verr, "spmm");
+  return (h & (TCSL_FLAG_DUPLICATE_LOCATIONS | TCSL_FLAG_PARTIAL_GROUPS)) == 0;
+}
+
+FloatMatrix spmm_device(const std::uint32_t* off, const std::uint32_t* ent, std::uint64_t n_entries, std::uint32_t m,
+                        std::uint32_t k, const TileConfig& cfg, bool tc_ready, const HalfMatrix& b,
+                        const SpmmOptions& opt) {
+  if (b.rows() <= 0 || b.cols() <= 0) raise(Errc::invalid_argument, "B must be non-empty");
+  if (static_cast<std::int64_t>(k) != b.rows())
+    raise(Errc::dimension_mismatch, "A has " + std::to_string(k) + " columns, B has " + std::to_string(b.rows()) +
+                                        " rows");
   const int n = static_cast<int>(b.cols());
-  FloatMatrix c(a.m, n);
-  const DeviceTcsl d = upload(a);
+  FloatMatrix c(m, n);
   Scratch& s = scratch();
-  // The reference accepts tiles whose spans are not whole 32-entry groups and
-  // locations repeated inside a tile (last writer wins, engine.cpp:8-25); the
-  // tensor-core decoders need neither. One device pass over the uploaded entries
-  // finds out, and such matrices take the bit-exact path, which handles both.
-  bool exact = opt.exact;
-  if (!exact && a.cfg.m_tb == 128 && a.cfg.k_tb == 64) {
-    auto* flags = static_cast<std::uint32_t*>(s.flags.get(sizeof(std::uint32_t)));
-    check(tcsl_cuda_memset(flags, 0, sizeof(std::uint32_t), nullptr), "memset");
-    int* verr = fresh_error_word();
-    check(tcsl_cuda_validate_entries(d.off, d.ent, a.entries.size(), a.m, a.k, a.cfg.m_tb, a.cfg.k_tb, TCSL_CHECK_SPMM,
-                                     flags, verr, nullptr),
-          "spmm");
-    std::uint32_t h = 0;
-    check(tcsl_cuda_memcpy_d2h(&h, flags, sizeof h, nullptr), "spmm");
-    collect_errors(verr, "spmm");
-    exact = (h & (TCSL_FLAG_DUPLICATE_LOCATIONS | TCSL_FLAG_PARTIAL_GROUPS)) != 0;
-  }
+  const bool exact = opt.exact || !tc_ready;
   const std::uint16_t* x = upload_half(s.x, b);
-  auto* y = static_cast<float*>(s.y.get(4ull * a.m * n));
+  auto* y = static_cast<float*>(s.y.get(4ull * m * n));
   std::size_t ws_bytes = 0;
   if (exact)
-    check(tcsl_cuda_spmm_exact_workspace(a.m, a.k, &ws_bytes), "spmm");
+    check(tcsl_cuda_spmm_exact_workspace(m, k, &ws_bytes), "spmm");
   else
-    check(tcsl_cuda_spmm_workspace(a.m, a.k, a.cfg.m_tb, a.cfg.k_tb, n, opt.split_k, &ws_bytes), "spmm");
+    check(tcsl_cuda_spmm_workspace(m, k, cfg.m_tb, cfg.k_tb, n, opt.split_k, &ws_bytes), "spmm");
   void* ws = s.ws.get(std::max<std::size_t>(ws_bytes, 256));
   int* err = fresh_error_word();
   if (exact)
-    check(tcsl_cuda_spmm_exact(d.off, d.ent, a.entries.size(), a.m, a.k, a.cfg.m_tb, a.cfg.k_tb, x, n, y, ws,
-                               ws_bytes, err, nullptr),
+    check(tcsl_cuda_spmm_exact(off, ent, n_entries, m, k, cfg.m_tb, cfg.k_tb, x, n, y, ws, ws_bytes, err, nullptr),
           "spmm");
   else
-    check(tcsl_cuda_spmm(d.off, d.ent, a.entries.size(), a.m, a.k, a.cfg.m_tb, a.cfg.k_tb, x, n, y, opt.split_k, ws,
-                         ws_bytes, err, nullptr),
+    check(tcsl_cuda_spmm(off, ent, n_entries, m, k, cfg.m_tb, cfg.k_tb, x, n, y, opt.split_k, ws, ws_bytes, err,
+                         nullptr),
           "spmm");
-  check(tcsl_cuda_memcpy_d2h(c.data(), y, 4ull * a.m * n, nullptr), "spmm");
+  check(tcsl_cuda_memcpy_d2h(c.data(), y, 4ull * m * n, nullptr), "spmm");
   collect_errors(err, "spmm");
   return c;
+}
+
+}  // namespace
+
+FloatMatrix spmm(const TcslMatrix& a, const HalfMatrix& b, const SpmmOptions& opt) {
+  check_spmm_args(a);
+  if (b.rows() <= 0 || b.cols() <= 0) raise(Errc::invalid_argument, "B must be non-empty");
+  if (static_cast<std::int64_t>(a.k) != b.rows())
+    raise(Errc::dimension_mismatch,
+          "A has " + std::to_string(a.k) + " columns, B has " + std::to_string(b.rows()) + " rows");
+  const DeviceTcsl d = upload(a);
+  const bool tc_ready = !opt.exact && tc_preconditions(d.off, d.ent, a.entries.size(), a.m, a.k, a.cfg);
+  return spmm_device(d.off, d.ent, a.entries.size(), a.m, a.k, a.cfg, tc_ready, b, opt);
+}
+
+DeviceMatrix::DeviceMatrix(const TcslMatrix& t) : m_(t.m), k_(t.k), cfg_(t.cfg), n_entries_(t.entries.size()) {
+  check_spmm_args(t);
+  check(tcsl_cuda_malloc(&off_, 4 * t.tile_offsets.size()), "device allocation");
+  check(tcsl_cuda_malloc(&ent_, 4 * std::max<std::size_t>(t.entries.size(), 1)), "device allocation");
+  check(tcsl_cuda_memcpy_h2d(off_, t.tile_offsets.data(), 4 * t.tile_offsets.size(), nullptr), "upload offsets");
+  check(tcsl_cuda_memcpy_h2d(ent_, t.entries.data(), 4 * t.entries.size(), nullptr), "upload entries");
+  tc_ready_ = tc_preconditions(static_cast<const std::uint32_t*>(off_), static_cast<const std::uint32_t*>(ent_),
+                                n_entries_, m_, k_, cfg_);
+}
+
+DeviceMatrix::~DeviceMatrix() {
+  tcsl_cuda_free(off_);
+  tcsl_cuda_free(ent_);
+}
+
+FloatMatrix DeviceMatrix::spmm(const HalfMatrix& b, const SpmmOptions& opt) const {
+  return spmm_device(static_cast<const std::uint32_t*>(off_), static_cast<const std::uint32_t*>(ent_), n_entries_,
+                     m_, k_, cfg_, tc_ready_, b, opt);
 }
 
 int reg_pressure(const TcslMatrix& t) {

@@ -9,6 +9,7 @@
 #include <random>
 #include <string>
 
+#include "tcsl/device.hpp"
 #include "tcsl/engine.hpp"
 #include "tcsl/gemm.hpp"
 #include "tcsl/tcsl_format.hpp"
@@ -212,6 +213,26 @@ int main() {
         for (int y = 0; y < 64; ++y) dense(r0 + x, c0 + y) = half_from_bits(d[static_cast<std::size_t>(x) * 64 + y]);
     }
     CHECK(same(decode(t), dense));
+  }
+
+  {  // weights-resident handle: the same bits as tcsl::spmm, call after call
+    const HalfMatrix a = gen_random_sparse(640, 1024, 0.8, 41);
+    const TcslMatrix t = encode(a);
+    const DeviceMatrix dm(t);
+    CHECK(dm.rows() == 640 && dm.cols() == 1024 && dm.entries() == t.entries.size() && dm.tensor_core_ready());
+    for (int n : {8, 24, 64}) {
+      const HalfMatrix b = gen_random_sparse(1024, n, 0.0, 42 + n);
+      CHECK(same(dm.spmm(b), spmm(t, b)));
+      CHECK(same(dm.spmm(b, SpmmOptions{3, false}), spmm(t, b, SpmmOptions{3, false})));
+      CHECK(same(dm.spmm(b, SpmmOptions{0, true}), dense_gemm_ref(decode(t), b)));
+    }
+    CHECK(thrown([&] { (void)dm.spmm(gen_random_sparse(1000, 8, 0.0, 2)); }) == Errc::dimension_mismatch);
+    TcslMatrix dup = t;  // a repeated location: the handle routes every call to the bit-exact path
+    dup.entries[1] = TcslEntry::make(dup.entries[1].value_bits(), dup.entries[0].location());
+    const DeviceMatrix dd(dup);
+    CHECK(!dd.tensor_core_ready());
+    const HalfMatrix b = gen_random_sparse(1024, 16, 0.0, 43);
+    CHECK(same(dd.spmm(b), dense_gemm_ref(decode(dup), b)));
   }
 
   std::printf("%d passed, %d failed\n", g_pass, g_fail);

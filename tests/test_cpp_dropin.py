@@ -26,7 +26,7 @@ def test_dropin_builds_and_links():
     syms = subprocess.run(["nm", "-DC", os.path.join(LIB, "libtcsl.so")], capture_output=True, text=True).stdout
     for name in ("tcsl::encode(", "tcsl::decode(", "tcsl::spmm(", "tcsl::dense_gemm_ref(", "tcsl::serialize_tcsl(",
                  "tcsl::deserialize_tcsl(", "tcsl::extract_tile(", "tcsl::reg_pressure(", "tcsl::gen_random_sparse(",
-                 "tcsl::prune_magnitude("):
+                 "tcsl::prune_magnitude(", "tcsl::DeviceMatrix::DeviceMatrix(", "tcsl::DeviceMatrix::spmm("):
         assert name in syms, name
 
 
